@@ -1,0 +1,167 @@
+/*
+ * flexprefill.h -- C ABI of libflexprefill.so, a B200 (sm_100a) implementation
+ * of FlexPrefill sparse prefill attention (arXiv 2502.20766).
+ *
+ * Citations: P:n = line n of the paper source; A1..A22 = the
+ * readings of silent/ambiguous passages, listed in DESIGN.md §3.
+ *
+ * The method (Alg. 1 "Sparse Attention") runs per attention head:
+ *   (i)   pattern determination  (Alg. 2)            -> fp_plan
+ *   (ii)  sparse index selection (Alg. 3 P:340-369 / Alg. 4 P:377-403,
+ *         forced blocks and minimum budget P:451)                 -> fp_select
+ *   (iii) y = A(Q, K, V, S)                  -> fp_sparse_attn
+ * plus a same-library dense causal kernel (the speedup denominator)
+ *                                                                 -> fp_dense_causal_attn
+ *
+ * Conventions (all entry points):
+ *  - Batch 1, causal, bf16. Q and O are [heads][seq_len][head_dim] row-major,
+ *    K and V are [kv_heads][seq_len][head_dim] row-major, contiguous. Q head h
+ *    uses KV head floor(h * kv_heads / heads) (GQA, contiguous groups; A15).
+ *  - Every tensor / workspace pointer is a DEVICE pointer unless the name
+ *    says host. The caller owns all memory; the library never allocates, keeps
+ *    no per-call state, and only enqueues work on `stream` (no host syncs), so
+ *    fp_plan -> fp_select -> fp_sparse_attn is CUDA-graph capturable. Stages
+ *    communicate through the workspace; data-dependent sizes stay on device.
+ *  - Validation is synchronous and happens before anything is enqueued; an
+ *    invalid call enqueues nothing and returns a non-zero fp_status:
+ *      FP_ERR_NULL      a required pointer is NULL
+ *      FP_ERR_SHAPE     heads % kv_heads != 0, seq_len % block_size != 0,
+ *                       seq_len < block_size, head_dim != 128, block_size != 128
+ *      FP_ERR_RANGE     gamma <= 0 or NaN; tau outside [0,1] or NaN; min_budget < 0
+ *                       (gamma >= 1 is allowed and selects every causal block, A7)
+ *      FP_ERR_ALIGN     a tensor pointer is not 16-byte aligned (TMA requirement)
+ *      FP_ERR_WORKSPACE ws_bytes < fp_workspace_bytes(...)
+ *      FP_ERR_DEVICE    the current device is not compute capability 10.0
+ *      FP_ERR_CUDA      a launch failed; fp_last_cuda_error() has the cudaError_t
+ *    Asynchronous faults surface at the caller's next synchronisation.
+ *    Outputs are undefined after any error.
+ */
+#ifndef FLEXPREFILL_H_
+#define FLEXPREFILL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FP_OK = 0,
+  FP_ERR_NULL = 1,
+  FP_ERR_SHAPE = 2,
+  FP_ERR_RANGE = 3,
+  FP_ERR_ALIGN = 4,
+  FP_ERR_WORKSPACE = 5,
+  FP_ERR_DEVICE = 6,
+  FP_ERR_CUDA = 7
+} fp_status;
+
+/* Per-head selection statistics (fp_select). k_v / k_s: number of selected
+ * vertical / slash lines (K_v, K_s of Alg. 3), 0 for QA heads;
+ * k_qa: K of Alg. 4, 0 for VS heads; nnz_blocks: computed (q-block,
+ * k-block) pairs after forced blocks and minimum budget; budget_added: blocks
+ * added by the minimum budget (A12); mass_*: achieved estimated mass of
+ * the selected lines/blocks (fixed-point sum). */
+typedef struct {
+  int32_t k_v, k_s, k_qa, nnz_blocks, budget_added, pattern;
+  double mass_v, mass_s, mass_qa;
+} fp_select_stats;
+
+/* Device pointers into a workspace filled by fp_plan / fp_select (for tests
+ * and stage-wise parity; read-only for the caller). Shapes, n = seq_len,
+ * nb = n / 128:
+ *   a_v, a_s   fp32 [heads][n]       vertical / slash line scores
+ *   a_hat      fp32 [heads][nb]      true block distribution (A2)
+ *   a_bar      fp32 [heads][nb]      estimated block distribution
+ *   k_bar      fp32 [kv_heads][nb][128]  avg-pooled keys
+ *   q_bar      fp32 [heads][nb][128]     avg-pooled queries (QA heads only)
+ *   A_bar      fp32 [heads][nb(nb+1)/2]  flattened normalised pooled map
+ *              (row-major over qb, kb <= qb; QA heads only)
+ *   As         fp32 [heads][nb]      slash mass per block diagonal (A12)
+ *   sel_v, sel_s  int32 [heads][n]   selected vertical / slash lines, ascending
+ *   sel_qa     int32 [heads][nb(nb+1)/2]  selected flat QA indices, ascending
+ *   sel_count  int32 [heads][3]      (K_v, K_s, K_qa)
+ *   row_nnz_pre int32 [heads][nb]    blocks per row before the minimum budget
+ */
+typedef struct {
+  const float *a_v, *a_s, *a_hat, *a_bar, *k_bar, *q_bar, *A_bar, *As;
+  const int32_t *sel_v, *sel_s, *sel_qa, *sel_count, *row_nnz_pre;
+} fp_debug_ptrs;
+
+/* Bytes of device workspace needed by fp_plan/fp_select/fp_sparse_attn for
+ * this shape (0 if the shape is invalid). */
+size_t fp_workspace_bytes(int heads, int kv_heads, int seq_len, int head_dim, int block_size);
+
+/* Per-head capacity (int32 entries) of col_idx: nb * (nb + 1) / 2. */
+size_t fp_col_idx_capacity(int seq_len, int block_size);
+
+/* Stage (i): Alg. 2 for every head, plus the Vertical-Slash line scores of
+ * Alg. 3 from the same representative attention and, for Query-Aware
+ * heads, the pooled map of Alg. 4 (it is the last step that reads Q).
+ *   q, k      device bf16, layouts above (only the last 128 rows of each Q head
+ *             and all of K are read, plus all of Q for Query-Aware heads)
+ *   tau       pattern threshold, [0, 1]; QA iff D_JS < tau
+ *   ws        device workspace of ws_bytes >= fp_workspace_bytes(...)
+ *   pattern   device int32 [heads] out: 1 = query_specific (QA), 0 = vertical_slash
+ *   jsd       device fp32 [heads] out: D_JS = sqrt(JSD(a_bar || a_hat)), base 2 (A1)
+ */
+fp_status fp_plan(const void* q, const void* k, int heads, int kv_heads, int seq_len, int head_dim,
+                  int block_size, float tau, void* ws, size_t ws_bytes, int32_t* pattern,
+                  float* jsd, void* stream);
+
+/* Stage (ii): cumulative-attention selection for every head, then
+ * forced first/diagonal key blocks (A11) and the minimum budget
+ * (min_budget tokens per query-block row, 0 = off; A12). Reads the workspace
+ * written by fp_plan on the same stream.
+ *   gamma     cumulative threshold (0, 1); >= 1 selects all (A7)
+ *   row_ptr   device int32 [heads][nb + 1] out: per-head CSR row offsets
+ *   col_idx   device int32 [heads][fp_col_idx_capacity] out: key blocks of each
+ *             query-block row, ascending (the diagonal block is last)
+ *   stats     device fp_select_stats [heads] out, or NULL
+ */
+fp_status fp_select(int heads, int kv_heads, int seq_len, int head_dim, int block_size, float gamma,
+                    int min_budget, void* ws, size_t ws_bytes, int32_t* row_ptr, int32_t* col_idx,
+                    fp_select_stats* stats, void* stream);
+
+/* Stage (iii): y = softmax((Q K^T + M_S) / sqrt(d)) V over exactly the blocks
+ * in the CSR (intersected with j <= i), online softmax, GQA.
+ *   o         device bf16 [heads][seq_len][128] out
+ *   row_ptr, col_idx  the CSR from fp_select (or any CSR with kb <= qb, each row
+ *             containing its diagonal block qb, kb ascending)
+ *   ws        workspace (scheduler scratch)
+ */
+fp_status fp_sparse_attn(const void* q, const void* k, const void* v, void* o, int heads,
+                         int kv_heads, int seq_len, int head_dim, int block_size,
+                         const int32_t* row_ptr, const int32_t* col_idx, void* ws, size_t ws_bytes,
+                         void* stream);
+
+/* Dense causal attention A(Q, K, V) with the same kernel (every kb <= qb). */
+fp_status fp_dense_causal_attn(const void* q, const void* k, const void* v, void* o, int heads,
+                               int kv_heads, int seq_len, int head_dim, int block_size,
+                               void* ws, size_t ws_bytes, void* stream);
+
+/* The whole layer (Alg. 1) from HOST buffers: copies q/k/v host->device into
+ * the caller's device buffers (d_q, d_k, d_v), runs plan/select/attn, and
+ * copies the output back to o_host; everything enqueued on `stream` (the copy
+ * is asynchronous only if the host buffers are pinned). */
+fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_host, void* o_host,
+                        void* d_q, void* d_k, void* d_v, void* d_o, int heads, int kv_heads,
+                        int seq_len, int head_dim, int block_size, float gamma, float tau,
+                        int min_budget, void* ws, size_t ws_bytes, int32_t* pattern, float* jsd,
+                        int32_t* row_ptr, int32_t* col_idx, void* stream);
+
+/* Fill *out with device pointers into ws (no device work). */
+fp_status fp_debug_view(const void* ws, int heads, int kv_heads, int seq_len, int head_dim,
+                        int block_size, fp_debug_ptrs* out);
+
+/* Number of kernels fp_plan / fp_select / fp_sparse_attn enqueue per call. */
+int fp_kernels_per_layer(void);
+
+const char* fp_status_string(fp_status s);
+int fp_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLEXPREFILL_H_ */

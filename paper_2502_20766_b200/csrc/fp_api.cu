@@ -1,0 +1,226 @@
+// fp_api.cu -- the C ABI (include/flexprefill.h): validation, workspace
+// layout, TMA descriptors, and the enqueue of the three stages.
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "fp_internal.h"
+
+namespace fp {
+
+static thread_local int g_last_cuda_error = 0;
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_tile_map(CUtensorMap* map, const void* base, long long rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {128, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {128 * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static fp_status check_shape(int heads, int kv_heads, int seq_len, int head_dim, int block_size) {
+  if (heads <= 0 || kv_heads <= 0 || seq_len <= 0) return FP_ERR_SHAPE;
+  if (heads % kv_heads != 0) return FP_ERR_SHAPE;
+  if (head_dim != 128 || block_size != 128) return FP_ERR_SHAPE;
+  if (seq_len % block_size != 0 || seq_len < block_size) return FP_ERR_SHAPE;
+  if (seq_len > (1 << 20)) return FP_ERR_SHAPE;  // bitmap / index capacity limit
+  return FP_OK;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static fp_status check_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FP_ERR_DEVICE;
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) return FP_ERR_DEVICE;
+  return FP_OK;
+}
+
+static fp_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return FP_OK;
+  g_last_cuda_error = (int)e;
+  return FP_ERR_CUDA;
+}
+
+}  // namespace fp
+
+using namespace fp;
+
+extern "C" {
+
+size_t fp_workspace_bytes(int heads, int kv_heads, int seq_len, int head_dim, int block_size) {
+  if (check_shape(heads, kv_heads, seq_len, head_dim, block_size) != FP_OK) return 0;
+  return ws_layout(make_shape(heads, kv_heads, seq_len)).total;
+}
+
+size_t fp_col_idx_capacity(int seq_len, int block_size) {
+  if (block_size <= 0 || seq_len <= 0) return 0;
+  const size_t nb = (size_t)seq_len / block_size;
+  return nb * (nb + 1) / 2;
+}
+
+int fp_kernels_per_layer(void) { return 8 + 5 + 1; }
+
+fp_status fp_plan(const void* q, const void* k, int heads, int kv_heads, int seq_len, int head_dim,
+                  int block_size, float tau, void* ws, size_t ws_bytes, int32_t* pattern,
+                  float* jsd, void* stream) {
+  if (!q || !k || !ws) return FP_ERR_NULL;
+  fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
+  if (st) return st;
+  if (!(tau >= 0.f && tau <= 1.f)) return FP_ERR_RANGE;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(ws)) return FP_ERR_ALIGN;
+  const Shape s = make_shape(heads, kv_heads, seq_len);
+  const WsLayout L = ws_layout(s);
+  if (ws_bytes < L.total) return FP_ERR_WORKSPACE;
+  if ((st = check_device())) return st;
+  CUtensorMap qm, km;
+  if (!make_tile_map(&qm, q, (long long)heads * seq_len) ||
+      !make_tile_map(&km, k, (long long)kv_heads * seq_len))
+    return cuda_status(cudaErrorInvalidValue);
+  return cuda_status(launch_plan(s, L, ws, q, k, qm, km, tau, pattern, jsd,
+                                 static_cast<cudaStream_t>(stream)));
+}
+
+fp_status fp_select(int heads, int kv_heads, int seq_len, int head_dim, int block_size, float gamma,
+                    int min_budget, void* ws, size_t ws_bytes, int32_t* row_ptr, int32_t* col_idx,
+                    fp_select_stats* stats, void* stream) {
+  if (!ws || !row_ptr || !col_idx) return FP_ERR_NULL;
+  fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
+  if (st) return st;
+  if (!(gamma > 0.f) || isnan(gamma) || min_budget < 0) return FP_ERR_RANGE;
+  if (!aligned16(ws)) return FP_ERR_ALIGN;
+  const Shape s = make_shape(heads, kv_heads, seq_len);
+  const WsLayout L = ws_layout(s);
+  if (ws_bytes < L.total) return FP_ERR_WORKSPACE;
+  if ((st = check_device())) return st;
+  return cuda_status(launch_select(s, L, ws, gamma, min_budget, row_ptr, col_idx, stats,
+                                   static_cast<cudaStream_t>(stream)));
+}
+
+static fp_status attn_common(const void* q, const void* k, const void* v, void* o, int heads,
+                             int kv_heads, int seq_len, int head_dim, int block_size,
+                             const int32_t* row_ptr, const int32_t* col_idx, void* ws,
+                             size_t ws_bytes, void* stream, bool dense) {
+  if (!q || !k || !v || !o) return FP_ERR_NULL;
+  if (!dense && (!row_ptr || !col_idx)) return FP_ERR_NULL;
+  fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
+  if (st) return st;
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return FP_ERR_ALIGN;
+  (void)ws_bytes;
+  if ((st = check_device())) return st;
+  const Shape s = make_shape(heads, kv_heads, seq_len);
+  const WsLayout L = ws_layout(s);
+  CUtensorMap qm, km, vm;
+  if (!make_tile_map(&qm, q, (long long)heads * seq_len) ||
+      !make_tile_map(&km, k, (long long)kv_heads * seq_len) ||
+      !make_tile_map(&vm, v, (long long)kv_heads * seq_len))
+    return cuda_status(cudaErrorInvalidValue);
+  return cuda_status(launch_attn(s, L, ws, qm, km, vm, o, row_ptr, col_idx, dense,
+                                 static_cast<cudaStream_t>(stream)));
+}
+
+fp_status fp_sparse_attn(const void* q, const void* k, const void* v, void* o, int heads,
+                         int kv_heads, int seq_len, int head_dim, int block_size,
+                         const int32_t* row_ptr, const int32_t* col_idx, void* ws, size_t ws_bytes,
+                         void* stream) {
+  return attn_common(q, k, v, o, heads, kv_heads, seq_len, head_dim, block_size, row_ptr, col_idx,
+                     ws, ws_bytes, stream, false);
+}
+
+fp_status fp_dense_causal_attn(const void* q, const void* k, const void* v, void* o, int heads,
+                               int kv_heads, int seq_len, int head_dim, int block_size, void* ws,
+                               size_t ws_bytes, void* stream) {
+  return attn_common(q, k, v, o, heads, kv_heads, seq_len, head_dim, block_size, nullptr, nullptr,
+                     ws, ws_bytes, stream, true);
+}
+
+fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_host, void* o_host,
+                        void* d_q, void* d_k, void* d_v, void* d_o, int heads, int kv_heads,
+                        int seq_len, int head_dim, int block_size, float gamma, float tau,
+                        int min_budget, void* ws, size_t ws_bytes, int32_t* pattern, float* jsd,
+                        int32_t* row_ptr, int32_t* col_idx, void* stream) {
+  if (!q_host || !k_host || !v_host || !o_host || !d_q || !d_k || !d_v || !d_o) return FP_ERR_NULL;
+  fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
+  if (st) return st;
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  const size_t qbytes = (size_t)heads * seq_len * 128 * 2, kbytes = (size_t)kv_heads * seq_len * 128 * 2;
+  cudaError_t e;
+  if ((e = cudaMemcpyAsync(d_q, q_host, qbytes, cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d_k, k_host, kbytes, cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d_v, v_host, kbytes, cudaMemcpyHostToDevice, cs)) != cudaSuccess)
+    return cuda_status(e);
+  if ((st = fp_plan(d_q, d_k, heads, kv_heads, seq_len, head_dim, block_size, tau, ws, ws_bytes,
+                    pattern, jsd, stream)))
+    return st;
+  if ((st = fp_select(heads, kv_heads, seq_len, head_dim, block_size, gamma, min_budget, ws, ws_bytes,
+                      row_ptr, col_idx, nullptr, stream)))
+    return st;
+  if ((st = fp_sparse_attn(d_q, d_k, d_v, d_o, heads, kv_heads, seq_len, head_dim, block_size,
+                           row_ptr, col_idx, ws, ws_bytes, stream)))
+    return st;
+  return cuda_status(cudaMemcpyAsync(o_host, d_o, qbytes, cudaMemcpyDeviceToHost, cs));
+}
+
+fp_status fp_debug_view(const void* ws, int heads, int kv_heads, int seq_len, int head_dim,
+                        int block_size, fp_debug_ptrs* out) {
+  if (!ws || !out) return FP_ERR_NULL;
+  fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
+  if (st) return st;
+  const WsLayout L = ws_layout(make_shape(heads, kv_heads, seq_len));
+  void* w = const_cast<void*>(ws);
+  out->a_v = wsp<float>(w, L.a_v);
+  out->a_s = wsp<float>(w, L.a_s);
+  out->a_hat = wsp<float>(w, L.a_hat);
+  out->a_bar = wsp<float>(w, L.a_bar);
+  out->k_bar = wsp<float>(w, L.k_bar);
+  out->q_bar = wsp<float>(w, L.q_bar);
+  out->A_bar = wsp<float>(w, L.A_bar);
+  out->As = wsp<float>(w, L.As);
+  out->sel_v = wsp<int32_t>(w, L.sel_v);
+  out->sel_s = wsp<int32_t>(w, L.sel_s);
+  out->sel_qa = wsp<int32_t>(w, L.sel_qa);
+  out->sel_count = wsp<int32_t>(w, L.sel_count);
+  out->row_nnz_pre = wsp<int32_t>(w, L.row_nnz_pre);
+  return FP_OK;
+}
+
+const char* fp_status_string(fp_status s) {
+  switch (s) {
+    case FP_OK: return "ok";
+    case FP_ERR_NULL: return "null pointer";
+    case FP_ERR_SHAPE: return "invalid shape";
+    case FP_ERR_RANGE: return "parameter out of range";
+    case FP_ERR_ALIGN: return "pointer not 16-byte aligned";
+    case FP_ERR_WORKSPACE: return "workspace too small";
+    case FP_ERR_DEVICE: return "device is not sm_100 (B200)";
+    case FP_ERR_CUDA: return "CUDA launch error";
+  }
+  return "unknown status";
+}
+
+int fp_last_cuda_error(void) { return g_last_cuda_error; }
+
+}  // extern "C"

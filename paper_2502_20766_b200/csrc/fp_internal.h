@@ -1,0 +1,119 @@
+// fp_internal.h -- workspace layout and kernel launchers (host side).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/flexprefill.h"
+
+namespace fp {
+
+constexpr int kChunkTiles = 8;  // key tiles (128 keys) per representative-pass CTA
+
+struct Shape {
+  int H, G, n, nb, nchunks, g;  // g = H / G
+  long long tri;                // nb (nb + 1) / 2
+};
+
+inline Shape make_shape(int heads, int kv_heads, int seq_len) {
+  Shape s;
+  s.H = heads;
+  s.G = kv_heads;
+  s.n = seq_len;
+  s.nb = seq_len / 128;
+  s.nchunks = (s.nb + kChunkTiles - 1) / kChunkTiles;
+  s.g = heads / kv_heads;
+  s.tri = (long long)s.nb * (s.nb + 1) / 2;
+  return s;
+}
+
+// Byte offsets of every workspace region (each 256-B aligned).
+struct WsLayout {
+  size_t m_part, l_part;     // fp32 [H][nchunks][128]  pass-1 partial row max / sum (log2 domain)
+  size_t m_row, il_row;      // fp32 [H][128]           combined row max, 1/row sum
+  size_t a_v, a_s;           // fp32 [H][n]
+  size_t as_part;            // fp32 [H][nb][256]       per-key-tile slash partials
+  size_t a_hat, a_bar, As;   // fp32 [H][nb]
+  size_t k_bar;              // fp32 [G][nb][128]
+  size_t q_bar;              // fp32 [H][nb][128]
+  size_t A_bar;              // fp32 [H][tri]
+  size_t pattern;            // int32 [H]
+  size_t jsd;                // fp32 [H]
+  size_t sel_v, sel_s;       // int32 [H][n]
+  size_t sel_qa;             // int32 [H][tri]
+  size_t sel_count;          // int32 [H][4]
+  size_t sel_mass;           // uint64 [H][4] fixed-point mass (2^-60 units)
+  size_t vbits, dbits;       // uint32 [H][nbw]   vertical-block / slash-diagonal bitmaps
+  size_t rowbits;            // uint32 [H][nb][nbw] final row bitmaps
+  size_t row_nnz, row_nnz_pre;  // int32 [H][nb]
+  size_t budget_added;       // int32 [H][nb]
+  size_t sched;              // int32 [64] scheduler scratch
+  size_t total;
+  int nbw;                   // words per bitmap row
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+inline WsLayout ws_layout(const Shape& s) {
+  WsLayout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  const size_t H = s.H, G = s.G, n = s.n, nb = s.nb, tri = s.tri;
+  L.nbw = (s.nb + 31) / 32;
+  L.m_part = take(H * s.nchunks * 128 * 4);
+  L.l_part = take(H * s.nchunks * 128 * 4);
+  L.m_row = take(H * 128 * 4);
+  L.il_row = take(H * 128 * 4);
+  L.a_v = take(H * n * 4);
+  L.a_s = take(H * n * 4);
+  L.as_part = take(H * nb * 256 * 4);
+  L.a_hat = take(H * nb * 4);
+  L.a_bar = take(H * nb * 4);
+  L.As = take(H * nb * 4);
+  L.k_bar = take(G * nb * 128 * 4);
+  L.q_bar = take(H * nb * 128 * 4);
+  L.A_bar = take(H * tri * 4);
+  L.pattern = take(H * 4);
+  L.jsd = take(H * 4);
+  L.sel_v = take(H * n * 4);
+  L.sel_s = take(H * n * 4);
+  L.sel_qa = take(H * tri * 4);
+  L.sel_count = take(H * 4 * 4);
+  L.sel_mass = take(H * 4 * 8);
+  L.vbits = take(H * L.nbw * 4);
+  L.dbits = take(H * L.nbw * 4);
+  L.rowbits = take(H * nb * L.nbw * 4);
+  L.row_nnz = take(H * nb * 4);
+  L.row_nnz_pre = take(H * nb * 4);
+  L.budget_added = take(H * nb * 4);
+  L.sched = take(64 * 4);
+  L.total = off;
+  return L;
+}
+
+template <typename T>
+inline T* wsp(void* ws, size_t off) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
+}
+
+// 2D bf16 tensor map: rows x 128 columns, box 128 rows x 64 cols, SWIZZLE_128B.
+bool make_tile_map(CUtensorMap* map, const void* base, long long rows);
+
+// ---- launchers (return cudaGetLastError of their launches) ----
+cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void* q, const void* k,
+                        const CUtensorMap& qmap, const CUtensorMap& kmap, float tau,
+                        int32_t* pattern_out, float* jsd_out, cudaStream_t st);
+cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gamma, int min_budget,
+                          int32_t* row_ptr, int32_t* col_idx, fp_select_stats* stats,
+                          cudaStream_t st);
+cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const CUtensorMap& qmap,
+                        const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+                        const int32_t* row_ptr, const int32_t* col_idx, bool dense,
+                        cudaStream_t st);
+
+}  // namespace fp

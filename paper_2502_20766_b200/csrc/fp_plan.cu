@@ -1,0 +1,466 @@
+// fp_plan.cu -- stage (i) of FlexPrefill: sparse pattern search (Alg. 2,
+// P:299-327) plus the Vertical-Slash line scores of Alg. 3,
+// computed once from the same representative attention, and the
+// Query-Aware pooled map of Alg. 4 for QA heads.
+//
+// Kernels (one stream, no host sync):
+//   rep_pass<1>   N1a  S = Q^ K^T per (key chunk, head) on tcgen05 -> partial
+//                      row max / sum-exp; first head of each KV group also
+//                      writes the avg-pooled keys K_bar
+//   rep_stats         combine partials -> per-row max and 1/sum (fixed order)
+//   rep_pass<2>   N1b  S^T = K Q^T per (key chunk, head) -> p = softmax entries,
+//                      a_v (column sums) and per-tile slash (diagonal) partials
+//   slash_combine     a_s[o] from the overlapping tile partials (fixed order)
+//   block_sums        a_hat[kb] = sum of a_v over kb (A2); As[D] (A12)
+//   pattern_kernel N3 a_bar = softmax(avgpool(Q^) K_bar^T / sqrt d), D_JS, decision
+//   qbar_kernel   N4a avg-pooled Q per block (QA heads only)
+//   pooled_map    N4b A_bar row softmax over kb <= qb, / nb (QA heads only)
+#include <math.h>
+
+#include "fp_common.cuh"
+#include "fp_internal.h"
+
+namespace fp {
+
+namespace {
+
+constexpr int kRepThreads = 128;
+constexpr int kStages = 3;
+
+struct RepSmem {
+  // tiles first (1024-B aligned by the dynamic smem base alignment)
+  uint8_t qhat[kTileBytes];
+  uint8_t kst[kStages][kTileBytes];
+  uint64_t q_full;
+  uint64_t k_full[kStages];
+  uint64_t mma_done[2];
+  uint32_t tmem_base;
+  float m_row[128];
+  float il_row[128];
+};
+constexpr int kTStride = 129;  // pass-2 transpose buffer row stride (floats)
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// deterministic block reductions (fixed shuffle tree + fixed smem order)
+template <int NT>
+__device__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  if (lane_id() == 0) red[warp_id()] = v;
+  __syncthreads();
+  float t = 0.f;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NT / 32; ++w) t += red[w];
+    red[32] = t;
+  }
+  __syncthreads();
+  t = red[32];
+  __syncthreads();
+  return t;
+}
+template <int NT>
+__device__ double block_sum_d(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane_id() == 0) red[warp_id()] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < NT / 32; ++w) t += red[w];
+    red[32] = t;
+  }
+  __syncthreads();
+  t = red[32];
+  __syncthreads();
+  return t;
+}
+template <int NT>
+__device__ float block_max(float v, float* red) {
+  v = warp_max(v);
+  if (lane_id() == 0) red[warp_id()] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = -INFINITY;
+    for (int w = 0; w < NT / 32; ++w) t = fmaxf(t, red[w]);
+    red[32] = t;
+  }
+  __syncthreads();
+  float t = red[32];
+  __syncthreads();
+  return t;
+}
+
+// --------------------------------------------------------------------------
+// Representative pass. PASS 1: A = Q^ (128 rep rows), B = K tile -> TMEM
+// lane = rep row r, column = key. PASS 2: A = K tile, B = Q^ -> lane = key,
+// column = rep row r. Both are M=N=K=128 bf16 UMMAs on K-major SW128 tiles.
+template <int PASS>
+__global__ void __launch_bounds__(kRepThreads, 1)
+    rep_pass(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+             int H, int G, int n, int nb, int nchunks, float scale_log2, float* __restrict__ m_part,
+             float* __restrict__ l_part, const float* __restrict__ m_row,
+             const float* __restrict__ il_row, float* __restrict__ k_bar, float* __restrict__ a_v,
+             float* __restrict__ as_part) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // SWIZZLE_128B tiles need 1024-B aligned shared addresses
+  uint8_t* sbase = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  RepSmem& sm = *reinterpret_cast<RepSmem*>(sbase);
+  float* T = reinterpret_cast<float*>(sbase + sizeof(RepSmem));  // PASS 2 only
+
+  const int tid = threadIdx.x;
+  const int chunk = blockIdx.x, h = blockIdx.y;
+  const int g = h / (H / G);
+  const int t0 = chunk * kChunkTiles;
+  const int ntile = min(kChunkTiles, nb - t0);
+  const bool do_kbar = (PASS == 1) && (h % (H / G) == 0);
+
+  if (warp_id() == 0) tmem_alloc(&sm.tmem_base, 256);
+  if (tid == 0) {
+    tma_prefetch_desc(&qmap);
+    tma_prefetch_desc(&kmap);
+    mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(&sm.k_full[s], 1);
+    for (int b = 0; b < 2; ++b) mbar_init(&sm.mma_done[b], 1);
+    mbar_fence_init();
+  }
+  if (PASS == 2) {
+    sm.m_row[tid] = m_row[h * 128 + tid];
+    sm.il_row[tid] = il_row[h * 128 + tid];
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm.tmem_base;
+  constexpr uint32_t idesc = make_idesc_bf16(128, 128, false);
+
+  auto issue_mma = [&](int t) {
+    const int s = t % kStages, b = t & 1;
+    mbar_wait(&sm.k_full[s], (t / kStages) & 1);
+    tc_fence_after();
+    const uint32_t qa = smem_u32(sm.qhat), ka = smem_u32(sm.kst[s]);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint64_t ad = PASS == 1 ? sdesc_kmajor(qa, kk) : sdesc_kmajor(ka, kk);
+      uint64_t bd = PASS == 1 ? sdesc_kmajor(ka, kk) : sdesc_kmajor(qa, kk);
+      umma_bf16_ss(tbase + b * 128, ad, bd, idesc, kk > 0);
+    }
+    umma_commit(&sm.mma_done[b]);
+  };
+
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&sm.q_full, kTileBytes);
+    tma_load_tile(sm.qhat, &qmap, &sm.q_full, h * n + n - 128);
+    for (int s = 0; s < kStages && s < ntile; ++s) {
+      mbar_arrive_expect_tx(&sm.k_full[s], kTileBytes);
+      tma_load_tile(sm.kst[s], &kmap, &sm.k_full[s], g * n + (t0 + s) * 128);
+    }
+    mbar_wait(&sm.q_full, 0);
+    issue_mma(0);
+  }
+
+  float m_loc = -INFINITY, l_loc = 0.f;  // PASS 1 running row stats (log2 domain)
+
+  for (int t = 0; t < ntile; ++t) {
+    if (tid == 0 && t + 1 < ntile) issue_mma(t + 1);
+    const int b = t & 1;
+    const int tile = t0 + t;
+    mbar_wait(&sm.mma_done[b], (t >> 1) & 1);
+    tc_fence_after();
+
+    uint32_t v[128];
+    const uint32_t lane_base = (uint32_t)(warp_id() * 32);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld32(tmem_addr(tbase + b * 128, lane_base, c * 32), v + c * 32);
+    tmem_wait_ld();
+
+    if (PASS == 1) {
+      // lane = rep row r; key j = tile*128 + c visible iff j <= p_r = n-128+r
+      const int r = tid;
+      const bool last = (tile == nb - 1);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        float x = __uint_as_float(v[c]) * scale_log2;
+        if (last && c > r) x = -INFINITY;
+        v[c] = __float_as_uint(x);
+        mx = fmaxf(mx, x);
+      }
+      const float m_new = fmaxf(m_loc, mx);
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) sum += exp2f(__uint_as_float(v[c]) - m_new);
+      l_loc = l_loc * exp2f(m_loc - m_new) + sum;
+      m_loc = m_new;
+      if (do_kbar) {
+        // avg-pooled key of this block, dimension d = tid (fixed row order)
+        const uint8_t* kt = sm.kst[t % kStages];
+        float acc = 0.f;
+        for (int row = 0; row < 128; ++row)
+          acc += bf16_to_f32(*reinterpret_cast<const uint16_t*>(kt + sw128_offset(row, tid)));
+        k_bar[((size_t)g * nb + tile) * 128 + tid] = acc * (1.0f / 128.0f);
+      }
+    } else {
+      // lane = key j_local, column = rep row r
+      const int jl = tid;
+      const int j = tile * 128 + jl;
+      const bool last = (tile == nb - 1);
+      float colsum = 0.f;
+      float* Trow = T + jl * kTStride;
+#pragma unroll
+      for (int r = 0; r < 128; ++r) {
+        float x = __uint_as_float(v[r]) * scale_log2;
+        float p = exp2f(x - sm.m_row[r]) * sm.il_row[r];
+        if (last && jl > r) p = 0.f;
+        colsum += p;
+        Trow[r] = p;
+      }
+      a_v[(size_t)h * n + j] = colsum * (1.0f / 128.0f);
+      __syncthreads();
+      // slash partials: diagonal delta = r - jl in [-127, 127]
+      // offset o = p_r - j = (n - 128 - tile*128) + delta
+      float* out = as_part + ((size_t)h * nb + tile) * 256;
+      {
+        const int d1 = tid - 127;  // -127 .. 0
+        float s = 0.f;
+        for (int q = max(0, -d1); q < 128 - max(0, d1); ++q) s += T[q * kTStride + q + d1];
+        out[d1 + 127] = s;
+      }
+      if (tid < 127) {
+        const int d2 = tid + 1;  // 1 .. 127
+        float s = 0.f;
+        for (int q = 0; q < 128 - d2; ++q) s += T[q * kTStride + q + d2];
+        out[d2 + 127] = s;
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0 && t + kStages < ntile) {
+      const int s = t % kStages;
+      mbar_arrive_expect_tx(&sm.k_full[s], kTileBytes);
+      tma_load_tile(sm.kst[s], &kmap, &sm.k_full[s], g * n + (t0 + t + kStages) * 128);
+    }
+  }
+
+  if (PASS == 1) {
+    m_part[((size_t)h * nchunks + chunk) * 128 + tid] = m_loc;
+    l_part[((size_t)h * nchunks + chunk) * 128 + tid] = l_loc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc(tbase, 256);
+}
+
+// per-row softmax statistics from the chunk partials (fixed chunk order)
+__global__ void rep_stats(int nchunks, const float* __restrict__ m_part,
+                          const float* __restrict__ l_part, float* __restrict__ m_row,
+                          float* __restrict__ il_row) {
+  const int h = blockIdx.x, r = threadIdx.x;
+  const float* mp = m_part + (size_t)h * nchunks * 128 + r;
+  const float* lp = l_part + (size_t)h * nchunks * 128 + r;
+  float m = -INFINITY;
+  for (int c = 0; c < nchunks; ++c) m = fmaxf(m, mp[c * 128]);
+  float l = 0.f;
+  for (int c = 0; c < nchunks; ++c) l += lp[c * 128] * exp2f(mp[c * 128] - m);
+  m_row[h * 128 + r] = m;
+  il_row[h * 128 + r] = 1.0f / l;
+}
+
+// a_s[o] = (sum of the overlapping per-tile diagonal partials) / b  (A9)
+__global__ void slash_combine(int n, int nb, const float* __restrict__ as_part,
+                              float* __restrict__ a_s) {
+  const int h = blockIdx.y;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n) return;
+  const int q = n - 128 - o;  // base(kt) = n - 128 - 128 kt ; delta = o - base = 128 kt - q
+  int kt_hi = (q + 127) >= 0 ? (q + 127) / 128 : -1;
+  float s = 0.f;
+  for (int kt = kt_hi - 1; kt <= kt_hi; ++kt) {  // ascending kt
+    if (kt < 0 || kt >= nb) continue;
+    const int delta = 128 * kt - q;
+    if (delta < -127 || delta > 127) continue;
+    s += as_part[((size_t)h * nb + kt) * 256 + delta + 127];
+  }
+  a_s[(size_t)h * n + o] = s * (1.0f / 128.0f);
+}
+
+// a_hat[kb] = sum_{j in kb} a_v[j] (A2) and As[D] = sum_{o in block D} a_s[o] (A12)
+__global__ void block_sums(int n, int nb, const float* __restrict__ a_v,
+                           const float* __restrict__ a_s, float* __restrict__ a_hat,
+                           float* __restrict__ As) {
+  __shared__ float red[33];
+  const int kb = blockIdx.x, h = blockIdx.y;
+  const size_t i = (size_t)h * n + (size_t)kb * 128 + threadIdx.x;
+  float sv = block_sum<128>(a_v[i], red);
+  float ss = block_sum<128>(a_s[i], red);
+  if (threadIdx.x == 0) {
+    a_hat[(size_t)h * nb + kb] = sv;
+    As[(size_t)h * nb + kb] = ss;
+  }
+}
+
+// Alg. 2: a_bar, D_JS (base 2, A1), decision (strict <, A14)
+constexpr int kPatThreads = 256;
+__global__ void __launch_bounds__(kPatThreads) pattern_kernel(
+    const __nv_bfloat16* __restrict__ q, const float* __restrict__ k_bar,
+    const float* __restrict__ a_hat, int H, int G, int n, int nb, float scale, float tau,
+    float* __restrict__ a_bar, int32_t* __restrict__ pattern_ws, float* __restrict__ jsd_ws,
+    int32_t* __restrict__ pattern_out, float* __restrict__ jsd_out) {
+  extern __shared__ float psm[];  // qbar[128] | logits[nb] | red[33]
+  float* qbar = psm;
+  float* logit = psm + 128;
+  float* red = logit + nb;
+  const int h = blockIdx.x, g = h / (H / G);
+  const int tid = threadIdx.x;
+  if (tid < 128) {
+    const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + ((size_t)h * n + n - 128) * 128;
+    float acc = 0.f;
+    for (int r = 0; r < 128; ++r) acc += bf16_to_f32(qh[r * 128 + tid]);
+    qbar[tid] = acc * (1.0f / 128.0f);
+  }
+  __syncthreads();
+  const int w = warp_id(), ln = lane_id();
+  for (int kb = w; kb < nb; kb += kPatThreads / 32) {
+    const float4 kv = *reinterpret_cast<const float4*>(k_bar + ((size_t)g * nb + kb) * 128 + ln * 4);
+    float d = qbar[ln * 4] * kv.x + qbar[ln * 4 + 1] * kv.y + qbar[ln * 4 + 2] * kv.z +
+              qbar[ln * 4 + 3] * kv.w;
+    d = warp_sum(d);
+    if (ln == 0) logit[kb] = d * scale;
+  }
+  __syncthreads();
+  float mx = -INFINITY;
+  for (int kb = tid; kb < nb; kb += kPatThreads) mx = fmaxf(mx, logit[kb]);
+  mx = block_max<kPatThreads>(mx, red);
+  float se = 0.f;
+  for (int kb = tid; kb < nb; kb += kPatThreads) se += expf(logit[kb] - mx);
+  se = block_sum<kPatThreads>(se, red);
+  // JSD terms in fp64: D = sqrt(JSD) amplifies rounding near D = 0
+  double js = 0.0;
+  for (int kb = tid; kb < nb; kb += kPatThreads) {
+    const float ab = expf(logit[kb] - mx) / se;
+    a_bar[(size_t)h * nb + kb] = ab;
+    const double pa = ab, ph = a_hat[(size_t)h * nb + kb];
+    const double m = 0.5 * (pa + ph);
+    if (pa > 0.0) js += pa * log2(pa / m);
+    if (ph > 0.0) js += ph * log2(ph / m);
+  }
+  __shared__ double redd[33];
+  js = block_sum_d<kPatThreads>(js, redd);
+  if (tid == 0) {
+    const float D = (float)sqrt(fmax(0.0, 0.5 * js));
+    const int pat = (D < tau) ? 1 : 0;
+    pattern_ws[h] = pat;
+    jsd_ws[h] = D;
+    if (pattern_out) pattern_out[h] = pat;
+    if (jsd_out) jsd_out[h] = D;
+  }
+}
+
+// avg-pooled queries of Query-Aware heads (Alg. 4 line 1)
+__global__ void qbar_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pattern,
+                            int n, int nb, float* __restrict__ q_bar) {
+  const int qb = blockIdx.x, h = blockIdx.y;
+  if (pattern[h] != 1) return;
+  const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + ((size_t)h * n + (size_t)qb * 128) * 128;
+  float acc = 0.f;
+#pragma unroll 8
+  for (int r = 0; r < 128; ++r) acc += bf16_to_f32(qh[r * 128 + threadIdx.x]);
+  q_bar[((size_t)h * nb + qb) * 128 + threadIdx.x] = acc * (1.0f / 128.0f);
+}
+
+// A_bar[qb, kb <= qb] = softmax_row(scale * Qbar[qb] . Kbar[kb]) / nb  (A5)
+constexpr int kMapThreads = 256;
+__global__ void __launch_bounds__(kMapThreads) pooled_map(
+    const float* __restrict__ q_bar, const float* __restrict__ k_bar,
+    const int32_t* __restrict__ pattern, int H, int G, int nb, float scale,
+    float* __restrict__ A_bar) {
+  extern __shared__ float msm[];  // qv[128] | logit[nb] | red[33]
+  const int qb = blockIdx.x, h = blockIdx.y;
+  if (pattern[h] != 1) return;
+  const int g = h / (H / G);
+  float* qv = msm;
+  float* logit = msm + 128;
+  float* red = logit + nb;
+  const int tid = threadIdx.x;
+  if (tid < 128) qv[tid] = q_bar[((size_t)h * nb + qb) * 128 + tid];
+  __syncthreads();
+  const int w = warp_id(), ln = lane_id();
+  for (int kb = w; kb <= qb; kb += kMapThreads / 32) {
+    const float4 kv = *reinterpret_cast<const float4*>(k_bar + ((size_t)g * nb + kb) * 128 + ln * 4);
+    float d = qv[ln * 4] * kv.x + qv[ln * 4 + 1] * kv.y + qv[ln * 4 + 2] * kv.z + qv[ln * 4 + 3] * kv.w;
+    d = warp_sum(d);
+    if (ln == 0) logit[kb] = d * scale;
+  }
+  __syncthreads();
+  float mx = -INFINITY;
+  for (int kb = tid; kb <= qb; kb += kMapThreads) mx = fmaxf(mx, logit[kb]);
+  mx = block_max<kMapThreads>(mx, red);
+  float se = 0.f;
+  for (int kb = tid; kb <= qb; kb += kMapThreads) se += expf(logit[kb] - mx);
+  se = block_sum<kMapThreads>(se, red);
+  float* out = A_bar + (size_t)h * ((size_t)nb * (nb + 1) / 2) + (size_t)qb * (qb + 1) / 2;
+  const float inv_nb = 1.0f / (float)nb;
+  for (int kb = tid; kb <= qb; kb += kMapThreads) out[kb] = (expf(logit[kb] - mx) / se) * inv_nb;
+}
+
+}  // namespace
+
+size_t rep_smem_bytes(int pass) {
+  size_t b = sizeof(RepSmem);
+  if (pass == 2) b += (size_t)128 * kTStride * 4;
+  return b + 1024;  // slack for manual alignment
+}
+
+cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void* q, const void* k,
+                        const CUtensorMap& qmap, const CUtensorMap& kmap, float tau,
+                        int32_t* pattern_out, float* jsd_out, cudaStream_t st) {
+  static bool attr_done = false;
+  const size_t sm1 = rep_smem_bytes(1), sm2 = rep_smem_bytes(2);
+  if (!attr_done) {
+    cudaFuncSetAttribute(rep_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    cudaFuncSetAttribute(rep_pass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    attr_done = true;
+  }
+  const float scale = 1.0f / sqrtf(128.0f);
+  const float scale_log2 = scale * kLog2e;
+  float* m_part = wsp<float>(ws, L.m_part);
+  float* l_part = wsp<float>(ws, L.l_part);
+  float* m_row = wsp<float>(ws, L.m_row);
+  float* il_row = wsp<float>(ws, L.il_row);
+  dim3 grid(s.nchunks, s.H);
+  rep_pass<1><<<grid, kRepThreads, sm1, st>>>(qmap, kmap, s.H, s.G, s.n, s.nb, s.nchunks, scale_log2,
+                                              m_part, l_part, m_row, il_row,
+                                              wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_v),
+                                              wsp<float>(ws, L.as_part));
+  rep_stats<<<s.H, 128, 0, st>>>(s.nchunks, m_part, l_part, m_row, il_row);
+  rep_pass<2><<<grid, kRepThreads, sm2, st>>>(qmap, kmap, s.H, s.G, s.n, s.nb, s.nchunks, scale_log2,
+                                              m_part, l_part, m_row, il_row,
+                                              wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_v),
+                                              wsp<float>(ws, L.as_part));
+  slash_combine<<<dim3((s.n + 255) / 256, s.H), 256, 0, st>>>(s.n, s.nb, wsp<float>(ws, L.as_part),
+                                                              wsp<float>(ws, L.a_s));
+  block_sums<<<dim3(s.nb, s.H), 128, 0, st>>>(s.n, s.nb, wsp<float>(ws, L.a_v),
+                                              wsp<float>(ws, L.a_s), wsp<float>(ws, L.a_hat),
+                                              wsp<float>(ws, L.As));
+  const size_t psm = (128 + (size_t)s.nb + 33) * 4;
+  pattern_kernel<<<s.H, kPatThreads, psm, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(q), wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_hat),
+      s.H, s.G, s.n, s.nb, scale, tau, wsp<float>(ws, L.a_bar), wsp<int32_t>(ws, L.pattern),
+      wsp<float>(ws, L.jsd), pattern_out, jsd_out);
+  qbar_kernel<<<dim3(s.nb, s.H), 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(q),
+                                               wsp<int32_t>(ws, L.pattern), s.n, s.nb,
+                                               wsp<float>(ws, L.q_bar));
+  pooled_map<<<dim3(s.nb, s.H), kMapThreads, psm, st>>>(
+      wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar), wsp<int32_t>(ws, L.pattern), s.H, s.G,
+      s.nb, scale, wsp<float>(ws, L.A_bar));
+  return cudaGetLastError();
+}
+
+}  // namespace fp

@@ -1,0 +1,474 @@
+// fp_select.cu -- stage (ii) of FlexPrefill: cumulative-attention index
+// selection (Alg. 3; Alg. 4), forced first /
+// diagonal key blocks and the minimum budget, emitted as a per-head
+// block CSR for the attention kernel.
+//
+// Kernels:
+//   topmass      N5  per segment (a_v, a_s of VS heads; flattened A_bar of QA
+//                    heads): MSD radix *select by mass* on the fp32 bit
+//                    patterns (11/11/10-bit digits) -> the threshold value
+//                    lambda (Appendix B), ties -> lower index (A8),
+//                    then an ordered compaction of the selected indices.
+//                    Masses are summed in 2^-60 fixed point (uint64), so every
+//                    sum is exact and order independent (deterministic).
+//   build_lines  N6a vertical-block / slash-diagonal bitmaps (A10, R1)
+//   assemble     N6b per query-block row: rasterised lines or QA blocks,
+//                    forced blocks (A11), minimum budget (A12)
+//   row_scan     N6c per-head CSR row offsets + stats
+//   write_cols   N6d CSR column indices (ascending kb)
+#include <math.h>
+
+#include "fp_common.cuh"
+#include "fp_internal.h"
+
+namespace fp {
+
+namespace {
+
+constexpr int kSelThreads = 1024;
+constexpr int kItems = 8;
+constexpr float kFixScale = 1152921504606846976.0f;  // 2^60
+
+__device__ __forceinline__ uint64_t fixp(float x) {
+  x = fminf(x, 8.0f);
+  return __float2ull_rz(x * kFixScale);
+}
+
+// block-wide inclusive scan of uint64 (1024 threads), returns inclusive value,
+// *total gets the block total. Deterministic (integer).
+__device__ uint64_t block_scan_u64(uint64_t v, uint64_t* wsum, uint64_t* total) {
+  const int ln = lane_id(), w = warp_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t y = __shfl_up_sync(0xffffffffu, v, o);
+    if (ln >= o) v += y;
+  }
+  if (ln == 31) wsum[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    uint64_t s = wsum[ln];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (ln >= o) s += y;
+    }
+    wsum[ln] = s;  // inclusive prefix of warp totals
+  }
+  __syncthreads();
+  uint64_t add = (w > 0) ? wsum[w - 1] : 0;
+  const uint64_t tot = wsum[31];
+  __syncthreads();
+  *total = tot;
+  return v + add;
+}
+
+struct TopSmem {
+  uint32_t cnt[2048];
+  unsigned long long mass[2048];
+  uint64_t wsum[32];
+  // selection state
+  uint32_t prefix;
+  uint32_t found_bin;
+  unsigned long long above_mass, above_cnt;
+  unsigned long long bin_mass, bin_cnt;
+  unsigned long long red[32];
+};
+
+// topmass(x, gamma) of one segment; see file header.
+__global__ void __launch_bounds__(kSelThreads, 1)
+    topmass_kernel(const float* __restrict__ a_v, const float* __restrict__ a_s,
+                   const float* __restrict__ A_bar, const int32_t* __restrict__ pattern, int n,
+                   long long tri, float gamma, int32_t* __restrict__ sel_v,
+                   int32_t* __restrict__ sel_s, int32_t* __restrict__ sel_qa,
+                   int32_t* __restrict__ sel_count, unsigned long long* __restrict__ sel_mass) {
+  __shared__ TopSmem sm;
+  const int seg = blockIdx.x, h = blockIdx.y;
+  const int pat = pattern[h];
+  if ((pat == 1) != (seg == 2)) {
+    if (threadIdx.x == 0) {
+      sel_count[h * 4 + seg] = 0;
+      sel_mass[h * 4 + seg] = 0;
+    }
+    return;
+  }
+  const float* x;
+  int32_t* out;
+  long long L;
+  if (seg == 0) {
+    x = a_v + (size_t)h * n;
+    out = sel_v + (size_t)h * n;
+    L = n;
+  } else if (seg == 1) {
+    x = a_s + (size_t)h * n;
+    out = sel_s + (size_t)h * n;
+    L = n;
+  } else {
+    x = A_bar + (size_t)h * tri;
+    out = sel_qa + (size_t)h * tri;
+    L = tri;
+  }
+  const int tid = threadIdx.x;
+
+  // ---- total mass T (fixed point, exact)
+  unsigned long long t_loc = 0;
+  for (long long i = tid; i < L; i += kSelThreads) t_loc += fixp(x[i]);
+  for (int o = 16; o > 0; o >>= 1) t_loc += __shfl_xor_sync(0xffffffffu, t_loc, o);
+  if (lane_id() == 0) sm.red[warp_id()] = t_loc;
+  __syncthreads();
+  unsigned long long T = 0;
+  for (int w = 0; w < 32; ++w) T += sm.red[w];
+
+  if (gamma >= 1.0f) {  // A7: gamma >= 1 selects everything
+    for (long long i = tid; i < L; i += kSelThreads) out[i] = (int32_t)i;
+    if (tid == 0) {
+      sel_count[h * 4 + seg] = (int32_t)L;
+      sel_mass[h * 4 + seg] = T;
+    }
+    return;
+  }
+  // K = min{k : C_k >= gamma T}  (A6, A7); G == 0 -> K = 1 (count mode)
+  const unsigned long long G = (unsigned long long)ceil((double)gamma * (double)T);
+  const bool count_mode = (G == 0);
+  unsigned long long rem = count_mode ? 1ull : G;
+
+  uint32_t prefix = 0, pmask = 0;
+  unsigned long long above_mass_tot = 0, above_cnt_tot = 0;
+  const int shifts[3] = {21, 10, 0};
+  const int widths[3] = {11, 11, 10};
+  for (int pass = 0; pass < 3; ++pass) {
+    const int sh = shifts[pass];
+    const uint32_t dmask = (1u << widths[pass]) - 1u;
+    const int nbins = 1 << widths[pass];
+    for (int b = tid; b < 2048; b += kSelThreads) {
+      sm.cnt[b] = 0;
+      sm.mass[b] = 0;
+    }
+    __syncthreads();
+    for (long long base = 0; base < L; base += kSelThreads) {
+      const long long i = base + tid;
+      const bool valid = i < L;
+      uint32_t key = valid ? __float_as_uint(x[i]) : 0xffffffffu;
+      const bool match = valid && ((key & pmask) == prefix);
+      const uint32_t digit = match ? ((key >> sh) & dmask) : 0xffffffffu;
+      const uint32_t grp = __match_any_sync(0xffffffffu, digit);
+      if (match) {
+        const uint64_t f = fixp(__uint_as_float(key));
+        const uint32_t c0 = (uint32_t)(f & 0xFFFFF), c1 = (uint32_t)((f >> 20) & 0xFFFFF),
+                       c2 = (uint32_t)(f >> 40);
+        const uint32_t s0 = __reduce_add_sync(grp, c0);
+        const uint32_t s1 = __reduce_add_sync(grp, c1);
+        const uint32_t s2 = __reduce_add_sync(grp, c2);
+        if ((__ffs(grp) - 1) == (int)lane_id()) {
+          atomicAdd(&sm.cnt[digit], (uint32_t)__popc(grp));
+          atomicAdd(&sm.mass[digit], ((unsigned long long)s2 << 40) +
+                                         ((unsigned long long)s1 << 20) + (unsigned long long)s0);
+        }
+      }
+    }
+    __syncthreads();
+    // descending-digit scan: thread t owns digits nbins-1-2t and nbins-2-2t
+    const int d0 = nbins - 1 - 2 * tid, d1 = d0 - 1;
+    uint64_t m0 = 0, m1 = 0, k0 = 0, k1 = 0;
+    if (d0 >= 0) {
+      m0 = sm.mass[d0];
+      k0 = sm.cnt[d0];
+    }
+    if (d1 >= 0) {
+      m1 = sm.mass[d1];
+      k1 = sm.cnt[d1];
+    }
+    uint64_t tot;
+    const uint64_t key_m = count_mode ? (k0 + k1) : (m0 + m1);
+    const uint64_t incl = block_scan_u64(key_m, sm.wsum, &tot);
+    const uint64_t excl = incl - key_m;
+    // second scan for the other quantity (mass when counting, count when massing)
+    const uint64_t other = count_mode ? (m0 + m1) : (k0 + k1);
+    const uint64_t incl_o = block_scan_u64(other, sm.wsum, &tot);
+    const uint64_t excl_o = incl_o - other;
+    // crossing: above < rem <= above + bin
+    {
+      const uint64_t q0 = count_mode ? k0 : m0, q1 = count_mode ? k1 : m1;
+      const uint64_t o0 = count_mode ? m0 : k0;
+      if (d0 >= 0 && excl < rem && rem <= excl + q0) {
+        sm.found_bin = d0;
+        sm.above_mass = count_mode ? excl_o : excl;
+        sm.above_cnt = count_mode ? excl : excl_o;
+        sm.bin_mass = m0;
+        sm.bin_cnt = k0;
+      } else if (d1 >= 0 && excl + q0 < rem && rem <= excl + q0 + q1) {
+        sm.found_bin = d1;
+        sm.above_mass = count_mode ? excl_o + o0 : excl + q0;
+        sm.above_cnt = count_mode ? excl + q0 : excl_o + o0;
+        sm.bin_mass = m1;
+        sm.bin_cnt = k1;
+      }
+    }
+    __syncthreads();
+    const uint32_t B = sm.found_bin;
+    prefix |= B << sh;
+    pmask |= dmask << sh;
+    above_mass_tot += sm.above_mass;
+    above_cnt_tot += sm.above_cnt;
+    rem -= count_mode ? sm.above_cnt : sm.above_mass;
+    __syncthreads();
+  }
+  // lambda = prefix; take t of its ties (lowest indices first)
+  const uint32_t lam = prefix;
+  const uint64_t f_lam = fixp(__uint_as_float(lam));
+  const uint64_t t_take = count_mode ? rem : (rem + f_lam - 1) / f_lam;
+  const uint64_t K = above_cnt_tot + t_take;
+
+  // ordered compaction: selected = key > lam, or key == lam among the first t_take ties
+  uint64_t gt_run = 0, eq_run = 0;
+  for (long long base = 0; base < L; base += (long long)kSelThreads * kItems) {
+    const long long i0 = base + (long long)tid * kItems;
+    uint32_t keys[kItems];
+    uint32_t gt = 0, eq = 0;
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const long long i = i0 + u;
+      keys[u] = (i < L) ? __float_as_uint(x[i]) : 0u;
+      const bool valid = i < L;
+      gt += (valid && keys[u] > lam);
+      eq += (valid && keys[u] == lam);
+    }
+    uint64_t tot;
+    const uint64_t packed = ((uint64_t)eq << 32) | gt;
+    const uint64_t incl = block_scan_u64(packed, sm.wsum, &tot);
+    const uint64_t excl = incl - packed;
+    uint64_t eq_pre = eq_run + (excl >> 32);
+    uint64_t pos = gt_run + (excl & 0xffffffffu) + min(t_take, eq_pre);
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const long long i = i0 + u;
+      if (i >= L) break;
+      bool take = keys[u] > lam;
+      if (keys[u] == lam) {
+        take = eq_pre < t_take;
+        ++eq_pre;
+      }
+      if (take) out[pos++] = (int32_t)i;
+    }
+    gt_run += tot & 0xffffffffu;
+    eq_run += tot >> 32;
+  }
+  if (tid == 0) {
+    sel_count[h * 4 + seg] = (int32_t)K;
+    sel_mass[h * 4 + seg] = above_mass_tot + t_take * f_lam;
+  }
+}
+
+// vertical-block and slash-diagonal bitmaps of VS heads (A10, reading R1)
+__global__ void build_lines(const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_v,
+                            const int32_t* __restrict__ sel_s, const int32_t* __restrict__ sel_count,
+                            int n, int nb, int nbw, uint32_t* __restrict__ vbits,
+                            uint32_t* __restrict__ dbits) {
+  extern __shared__ uint32_t bsm[];  // V[nbw] | D[nbw]
+  const int h = blockIdx.x;
+  uint32_t* V = bsm;
+  uint32_t* Dg = bsm + nbw;
+  for (int w = threadIdx.x; w < 2 * nbw; w += blockDim.x) bsm[w] = 0;
+  __syncthreads();
+  if (pattern[h] == 0) {
+    const int kv = sel_count[h * 4 + 0], ks = sel_count[h * 4 + 1];
+    const int32_t* sv = sel_v + (size_t)h * n;
+    const int32_t* ss = sel_s + (size_t)h * n;
+    for (int i = threadIdx.x; i < kv; i += blockDim.x) {
+      const int kb = sv[i] >> 7;
+      atomicOr(&V[kb >> 5], 1u << (kb & 31));
+    }
+    for (int i = threadIdx.x; i < ks; i += blockDim.x) {
+      const int o = ss[i];
+      const int d = o >> 7;
+      atomicOr(&Dg[d >> 5], 1u << (d & 31));
+      if ((o & 127) && d + 1 < nb) atomicOr(&Dg[(d + 1) >> 5], 1u << ((d + 1) & 31));
+    }
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < nbw; w += blockDim.x) {
+    vbits[(size_t)h * nbw + w] = V[w];
+    dbits[(size_t)h * nbw + w] = Dg[w];
+  }
+}
+
+__device__ __forceinline__ bool bit_at(const uint32_t* b, int i) { return (b[i >> 5] >> (i & 31)) & 1u; }
+
+// one warp per (head, query-block row)
+constexpr int kAsmWarps = 8;
+__global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows(
+    const int32_t* __restrict__ pattern, const uint32_t* __restrict__ vbits,
+    const uint32_t* __restrict__ dbits, const int32_t* __restrict__ sel_qa,
+    const int32_t* __restrict__ sel_count, const float* __restrict__ a_hat,
+    const float* __restrict__ As, const float* __restrict__ A_bar, int nb, int nbw,
+    long long tri, int min_blocks, uint32_t* __restrict__ rowbits, int32_t* __restrict__ row_nnz,
+    int32_t* __restrict__ row_nnz_pre, int32_t* __restrict__ budget_added) {
+  extern __shared__ uint32_t asmem[];  // [kAsmWarps][nbw]
+  const int h = blockIdx.y;
+  const int w = warp_id(), ln = lane_id();
+  const int qb = blockIdx.x * kAsmWarps + w;
+  if (qb >= nb) return;
+  uint32_t* row = asmem + w * nbw;
+  const int pat = pattern[h];
+  const uint32_t* V = vbits + (size_t)h * nbw;
+  const uint32_t* Dg = dbits + (size_t)h * nbw;
+  for (int i = ln; i < nbw; i += 32) row[i] = 0;
+  __syncwarp();
+  const int nw_row = (qb >> 5) + 1;  // words that can hold kb <= qb
+  if (pat == 0) {
+    for (int wd = 0; wd < nw_row; ++wd) {
+      const int kb = wd * 32 + ln;
+      const bool on = (kb <= qb) && (bit_at(V, kb) || bit_at(Dg, qb - kb));
+      const uint32_t word = __ballot_sync(0xffffffffu, on);
+      if (ln == 0) row[wd] = word;
+    }
+  } else {
+    // S_qa is sorted; this row's flat indices are [qb(qb+1)/2, qb(qb+1)/2 + qb]
+    const int kq = sel_count[h * 4 + 2];
+    const int32_t* sq = sel_qa + (size_t)h * tri;
+    const long long lo = (long long)qb * (qb + 1) / 2, hi = lo + qb;
+    // lower bound of lo (every lane does the same binary search)
+    int a = 0, b = kq;
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (sq[mid] < lo) a = mid + 1; else b = mid;
+    }
+    for (int i = a + ln; i < kq; i += 32) {
+      const long long p = sq[i];
+      if (p > hi) break;
+      const int kb = (int)(p - lo);
+      atomicOr(&row[kb >> 5], 1u << (kb & 31));
+    }
+  }
+  __syncwarp();
+  if (ln == 0) {
+    row[0] |= 1u;                       // first key block (A11)
+    row[qb >> 5] |= 1u << (qb & 31);    // diagonal = last key block of the row
+  }
+  __syncwarp();
+  int cnt = 0;
+  for (int wd = ln; wd < nw_row; wd += 32) cnt += __popc(row[wd]);
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  const int pre = cnt;
+  // minimum budget (A12): best unselected kb <= qb by row score, ties -> lower kb
+  const int need = min(min_blocks, qb + 1) - cnt;
+  const float* Ab = A_bar + (size_t)h * tri + (size_t)qb * (qb + 1) / 2;
+  for (int it = 0; it < need; ++it) {
+    float best = -INFINITY;
+    int bkb = 0x7fffffff;
+    for (int kb = ln; kb <= qb; kb += 32) {
+      if (bit_at(row, kb)) continue;
+      const float sc = (pat == 0) ? __fadd_rn(a_hat[(size_t)h * nb + kb], As[(size_t)h * nb + qb - kb])
+                                  : Ab[kb];
+      if (sc > best || (sc == best && kb < bkb)) {
+        best = sc;
+        bkb = kb;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ok = __shfl_xor_sync(0xffffffffu, bkb, o);
+      if (ob > best || (ob == best && ok < bkb)) {
+        best = ob;
+        bkb = ok;
+      }
+    }
+    if (ln == 0) row[bkb >> 5] |= 1u << (bkb & 31);
+    __syncwarp();
+  }
+  const int added = need > 0 ? need : 0;
+  uint32_t* dst = rowbits + ((size_t)h * nb + qb) * nbw;
+  for (int i = ln; i < nbw; i += 32) dst[i] = row[i];
+  if (ln == 0) {
+    row_nnz[(size_t)h * nb + qb] = pre + added;
+    row_nnz_pre[(size_t)h * nb + qb] = pre;
+    budget_added[(size_t)h * nb + qb] = added;
+  }
+}
+
+// exclusive scan of row nnz per head -> row_ptr; stats
+__global__ void __launch_bounds__(kSelThreads, 1)
+    row_scan(const int32_t* __restrict__ row_nnz, const int32_t* __restrict__ budget_added,
+             const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_count,
+             const unsigned long long* __restrict__ sel_mass, int nb, int32_t* __restrict__ row_ptr,
+             fp_select_stats* __restrict__ stats) {
+  __shared__ uint64_t wsum[32];
+  const int h = blockIdx.x;
+  uint64_t run = 0, badd = 0;
+  for (int base = 0; base < nb; base += kSelThreads) {
+    const int i = base + threadIdx.x;
+    const uint64_t v = (i < nb) ? (uint64_t)row_nnz[(size_t)h * nb + i] : 0;
+    const uint64_t ba = (i < nb) ? (uint64_t)budget_added[(size_t)h * nb + i] : 0;
+    uint64_t tot;
+    const uint64_t packed = (ba << 32) | v;
+    const uint64_t incl = block_scan_u64(packed, wsum, &tot);
+    if (i < nb) row_ptr[(size_t)h * (nb + 1) + i] = (int32_t)(run + ((incl - packed) & 0xffffffffu));
+    run += tot & 0xffffffffu;
+    badd += tot >> 32;
+  }
+  if (threadIdx.x == 0) {
+    row_ptr[(size_t)h * (nb + 1) + nb] = (int32_t)run;
+    if (stats) {
+      fp_select_stats st;
+      const double inv = 1.0 / 1152921504606846976.0;
+      st.pattern = pattern[h];
+      st.k_v = sel_count[h * 4 + 0];
+      st.k_s = sel_count[h * 4 + 1];
+      st.k_qa = sel_count[h * 4 + 2];
+      st.mass_v = (double)sel_mass[h * 4 + 0] * inv;
+      st.mass_s = (double)sel_mass[h * 4 + 1] * inv;
+      st.mass_qa = (double)sel_mass[h * 4 + 2] * inv;
+      st.nnz_blocks = (int32_t)run;
+      st.budget_added = (int32_t)badd;
+      stats[h] = st;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kAsmWarps * 32) write_cols(
+    const uint32_t* __restrict__ rowbits, const int32_t* __restrict__ row_ptr, int nb, int nbw,
+    long long cap, int32_t* __restrict__ col_idx) {
+  const int h = blockIdx.y;
+  const int w = warp_id(), ln = lane_id();
+  const int qb = blockIdx.x * kAsmWarps + w;
+  if (qb >= nb) return;
+  const uint32_t* row = rowbits + ((size_t)h * nb + qb) * nbw;
+  int32_t* out = col_idx + (size_t)h * cap + row_ptr[(size_t)h * (nb + 1) + qb];
+  int pos = 0;
+  const int nw_row = (qb >> 5) + 1;
+  for (int wd = 0; wd < nw_row; ++wd) {
+    const uint32_t word = row[wd];
+    if ((word >> ln) & 1u) out[pos + __popc(word & ((1u << ln) - 1u))] = wd * 32 + ln;
+    pos += __popc(word);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gamma, int min_budget,
+                          int32_t* row_ptr, int32_t* col_idx, fp_select_stats* stats,
+                          cudaStream_t st) {
+  const int32_t* pat = wsp<int32_t>(ws, L.pattern);
+  topmass_kernel<<<dim3(3, s.H), kSelThreads, 0, st>>>(
+      wsp<float>(ws, L.a_v), wsp<float>(ws, L.a_s), wsp<float>(ws, L.A_bar), pat, s.n, s.tri, gamma,
+      wsp<int32_t>(ws, L.sel_v), wsp<int32_t>(ws, L.sel_s), wsp<int32_t>(ws, L.sel_qa),
+      wsp<int32_t>(ws, L.sel_count), wsp<unsigned long long>(ws, L.sel_mass));
+  build_lines<<<s.H, 1024, 2 * L.nbw * 4, st>>>(pat, wsp<int32_t>(ws, L.sel_v),
+                                                wsp<int32_t>(ws, L.sel_s),
+                                                wsp<int32_t>(ws, L.sel_count), s.n, s.nb, L.nbw,
+                                                wsp<uint32_t>(ws, L.vbits), wsp<uint32_t>(ws, L.dbits));
+  const int min_blocks = (min_budget + 127) / 128;
+  const dim3 rg((s.nb + kAsmWarps - 1) / kAsmWarps, s.H);
+  assemble_rows<<<rg, kAsmWarps * 32, kAsmWarps * L.nbw * 4, st>>>(
+      pat, wsp<uint32_t>(ws, L.vbits), wsp<uint32_t>(ws, L.dbits), wsp<int32_t>(ws, L.sel_qa),
+      wsp<int32_t>(ws, L.sel_count), wsp<float>(ws, L.a_hat), wsp<float>(ws, L.As),
+      wsp<float>(ws, L.A_bar), s.nb, L.nbw, s.tri, min_blocks, wsp<uint32_t>(ws, L.rowbits),
+      wsp<int32_t>(ws, L.row_nnz), wsp<int32_t>(ws, L.row_nnz_pre), wsp<int32_t>(ws, L.budget_added));
+  row_scan<<<s.H, kSelThreads, 0, st>>>(wsp<int32_t>(ws, L.row_nnz), wsp<int32_t>(ws, L.budget_added),
+                                        pat, wsp<int32_t>(ws, L.sel_count),
+                                        wsp<unsigned long long>(ws, L.sel_mass), s.nb, row_ptr, stats);
+  write_cols<<<rg, kAsmWarps * 32, 0, st>>>(wsp<uint32_t>(ws, L.rowbits), row_ptr, s.nb, L.nbw,
+                                            s.tri, col_idx);
+  return cudaGetLastError();
+}
+
+}  // namespace fp

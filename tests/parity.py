@@ -1,0 +1,136 @@
+"""Parity checker: CUDA path (through the C ABI) vs the float64 oracle.
+
+Test infrastructure (may import oracle/). Implements SURVEY.md §8(c) "Parity
+rules": stage-wise checks (the oracle fed the GPU's own inputs to a stage)
+and the end-to-end borderline classifier with delta = 1e-5 (north_star:
+"bit-exact, except for blocks whose fp32 scores lie within 1e-5 of the
+cumulative threshold, which are reported separately").
+"""
+import numpy as np
+
+import oracle
+
+DELTA = 1e-5        # end-to-end borderline window on C_{k-1} - gamma T
+STAGE_DELTA = 1e-12  # stage-wise: summation-order ties only
+LAM_REL = 1e-5      # near-tie window around the K-th score (Appendix B lambda)
+
+
+def to_torch_bf16(bits, device="cuda"):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(bits)).view(torch.bfloat16).to(device)
+
+
+def run_gpu(fp, w, q_bits, k_bits, v_bits, gamma=None, tau=None, min_budget=None, dense=False,
+            want_out=True):
+    """Run plan -> select -> attn through the binding; return host copies."""
+    import torch
+    gamma = w.gamma if gamma is None else gamma
+    tau = w.tau if tau is None else tau
+    min_budget = w.min_budget if min_budget is None else min_budget
+    q, k, v = (to_torch_bf16(x) for x in (q_bits, k_bits, v_bits))
+    fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len)
+    fpl.plan(q, k, tau)
+    fpl.select(gamma, min_budget)
+    out = torch.empty_like(q)
+    if want_out:
+        fpl.attn(q, k, v, out)
+    res = dict(pattern=fpl.pattern.cpu().numpy(), jsd=fpl.jsd.cpu().numpy(),
+               row_ptr=fpl.row_ptr.cpu().numpy(), col_idx=fpl.col_idx.cpu().numpy(),
+               stats=fpl.stats(), dbg={k_: v_.numpy() for k_, v_ in fpl.debug().items()})
+    if want_out:
+        res["out"] = out.float().cpu().numpy()
+    if dense:
+        od = torch.empty_like(q)
+        fpl.dense(q, k, v, od)
+        res["dense"] = od.float().cpu().numpy()
+    torch.cuda.synchronize()
+    return res
+
+
+def csr_mask(row_ptr, col_idx, nb):
+    M = np.zeros((nb, nb), bool)
+    for qb in range(nb):
+        M[qb, col_idx[row_ptr[qb]:row_ptr[qb + 1]]] = True
+    return M
+
+
+def csr_rows_sorted(row_ptr, col_idx, nb):
+    for qb in range(nb):
+        r = col_idx[row_ptr[qb]:row_ptr[qb + 1]]
+        if not (np.all(np.diff(r) > 0) and r[-1] == qb and r[0] == 0 and np.all(r <= qb)):
+            return False
+    return True
+
+
+def classify(x, gamma, sel, delta=DELTA, lam_rel=LAM_REL):
+    """Compare a GPU index set `sel` with oracle topmass(x, gamma).
+
+    Element at oracle rank k (1-based) is selected exactly when C_{k-1} < gamma T.
+    in:  C_{k-1} < gamma T - delta;   out: C_{k-1} > gamma T + delta;
+    borderline: otherwise, or its score within lam_rel of the K-th score.
+    Returns (missing_in, extra_out, borderline_diffs, n_borderline).
+    """
+    t = oracle.topmass(x, gamma)
+    order, C = t["order"], t["C"]
+    L = len(x)
+    sel = np.asarray(sel, np.int64)
+    gsel = np.zeros(L, bool)
+    gsel[sel] = True
+    if gamma >= 1.0:
+        return int((~gsel).sum()), 0, 0, 0
+    G = gamma * t["T"]
+    Cprev = np.concatenate([[0.0], C[:-1]])  # C_{k-1} for rank k
+    lam = x[order[t["K"] - 1]]
+    xs = x[order]
+    border = (np.abs(Cprev - G) <= delta) | (np.abs(xs - lam) <= lam_rel * max(lam, 1e-300))
+    inn = (Cprev < G - delta) & ~border
+    out = (Cprev > G + delta) & ~border
+    inn[0] = inn[0] or not border[0]  # rank 1 is always selected
+    g = gsel[order]
+    missing_in = int((inn & ~g).sum())
+    extra_out = int((out & g).sum())
+    bdiff = int((border & (g != (Cprev < G))).sum())
+    return missing_in, extra_out, bdiff, int(border.sum())
+
+
+def oracle_inputs(q_bits, k_bits, v_bits):
+    from synth import gen
+    return gen.bits_to_f64(q_bits), gen.bits_to_f64(k_bits), gen.bits_to_f64(v_bits)
+
+
+def rel_close(a, b, rtol, floor):
+    """relative agreement on entries with |b| >= floor; absolute below."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    big = np.abs(b) >= floor
+    rel = np.abs(a - b)[big] / np.abs(b)[big] if big.any() else np.zeros(1)
+    small = np.abs(a - b)[~big]
+    return float(rel.max(initial=0.0)), float(small.max(initial=0.0))
+
+
+def stagewise_mask(pattern, dbg, h, n, gamma, min_budget, b=128):
+    """Oracle O6-O9 applied to the GPU's own line/QA sets and fp32 scores.
+
+    The minimum-budget order is decided in fp32 like the kernel (A12 score
+    a_hat[kb] + As[qb-kb] rounded to fp32; QA: A_bar in fp32)."""
+    nb = n // b
+    cnt = dbg["sel_count"][h]
+    if pattern == oracle.VS:
+        S_v = dbg["sel_v"][h, : cnt[0]]
+        S_s = dbg["sel_s"][h, : cnt[1]]
+        M0 = oracle.vs_block_mask(S_v, S_s, n, b)
+        ah = dbg["a_hat"][h].astype(np.float32)
+        As = dbg["As"][h].astype(np.float32)
+        qb = np.arange(nb)[:, None]
+        kb = np.arange(nb)[None, :]
+        R = (ah[kb] + As[np.clip(qb - kb, 0, nb - 1)]).astype(np.float32).astype(np.float64)
+        R = np.where(kb <= qb, R, -np.inf)
+    else:
+        vals, rows, cols = oracle.qa_flat(np.zeros((nb, nb)))
+        S_qa = dbg["sel_qa"][h, : cnt[2]]
+        M0 = oracle.qa_block_mask(S_qa, rows, cols, nb)
+        A = np.full((nb, nb), -np.inf)
+        A[rows, cols] = dbg["A_bar"][h, : len(rows)].astype(np.float64)
+        R = A
+    M1 = oracle.add_forced(M0)
+    return M0, oracle.min_budget_extend(M1, R, min_budget, b)

@@ -1,0 +1,82 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol
+include/flexprefill.h declares, sizes workspaces, and validates arguments
+(every validation error is returned before any device work is attempted)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2502_20766_b200 as fp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "flexprefill.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(fp.LIB_PATH):
+        from paper_2502_20766_b200 import build
+        build.build()
+    return fp.load_library()
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fp_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    syms = declared_symbols()
+    assert {"fp_plan", "fp_select", "fp_sparse_attn", "fp_dense_causal_attn"} <= set(syms)
+    raw = ctypes.CDLL(fp.LIB_PATH)
+    for s in syms:
+        assert hasattr(raw, s), s
+
+
+def test_workspace_and_capacity(lib):
+    assert fp.fp_col_idx_capacity(131072) == 1024 * 1025 // 2
+    b1 = fp.fp_workspace_bytes(32, 8, 32768)
+    b2 = fp.fp_workspace_bytes(32, 8, 131072)
+    assert 0 < b1 < b2 < (1 << 31)
+    for bad in [(32, 7, 32768), (32, 8, 1000), (32, 8, 64), (0, 1, 2048)]:
+        assert fp.fp_workspace_bytes(*bad) == 0
+    assert fp.fp_workspace_bytes(4, 1, 2048, head_dim=64) == 0
+    assert fp.fp_workspace_bytes(4, 1, 2048, block_size=64) == 0
+
+
+def test_validation_codes_without_device(lib):
+    ws_bytes = fp.fp_workspace_bytes(4, 1, 2048)
+    P = 0x10000  # fake, 16-B aligned; never dereferenced by validation
+    L = lib
+    s = ctypes.c_void_p(0)
+    assert L.fp_plan(None, P, 4, 1, 2048, 128, 128, 0.1, P, ws_bytes, P, P, s) == 1
+    assert L.fp_plan(P, P, 4, 3, 2048, 128, 128, 0.1, P, ws_bytes, P, P, s) == 2
+    assert L.fp_plan(P, P, 4, 1, 2000, 128, 128, 0.1, P, ws_bytes, P, P, s) == 2
+    assert L.fp_plan(P, P, 4, 1, 2048, 64, 128, 0.1, P, ws_bytes, P, P, s) == 2
+    assert L.fp_plan(P, P, 4, 1, 2048, 128, 128, -0.1, P, ws_bytes, P, P, s) == 3
+    assert L.fp_plan(P, P, 4, 1, 2048, 128, 128, float("nan"), P, ws_bytes, P, P, s) == 3
+    assert L.fp_plan(P + 8, P, 4, 1, 2048, 128, 128, 0.1, P, ws_bytes, P, P, s) == 4
+    assert L.fp_plan(P, P, 4, 1, 2048, 128, 128, 0.1, P, ws_bytes - 1, P, P, s) == 5
+    assert L.fp_select(4, 1, 2048, 128, 128, 0.0, 0, P, ws_bytes, P, P, None, s) == 3
+    assert L.fp_select(4, 1, 2048, 128, 128, 0.9, -1, P, ws_bytes, P, P, None, s) == 3
+    assert L.fp_select(4, 1, 2048, 128, 128, float("nan"), 0, P, ws_bytes, P, P, None, s) == 3
+    assert L.fp_select(4, 1, 2048, 128, 128, 0.9, 0, P, ws_bytes, None, P, None, s) == 1
+    assert L.fp_sparse_attn(P, P, P, P, 4, 1, 2048, 128, 128, None, P, P, ws_bytes, s) == 1
+    assert L.fp_sparse_attn(P, P, P, P + 4, 4, 1, 2048, 128, 128, P, P, P, ws_bytes, s) == 4
+    # all arguments valid: on a box without an sm_100 device -> FP_ERR_DEVICE
+    import torch
+    if not torch.cuda.is_available():
+        assert L.fp_plan(P, P, 4, 1, 2048, 128, 128, 0.1, P, ws_bytes, P, P, s) == 6
+        assert L.fp_dense_causal_attn(P, P, P, P, 4, 1, 2048, 128, 128, None, 0, s) == 6
+    for code in range(8):
+        assert L.fp_status_string(code)
+
+
+def test_binding_raises_without_fallback(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(Exception):
+        fp.FlexPrefill(4, 1, 2048)
