@@ -24,7 +24,7 @@ namespace fp {
 
 namespace {
 
-constexpr int kRepThreads = 128;
+constexpr int kRepThreads = 256;
 constexpr int kStages = 3;
 
 struct RepSmem {
@@ -37,6 +37,7 @@ struct RepSmem {
   uint32_t tmem_base;
   float m_row[128];
   float il_row[128];
+  float red[512];
 };
 constexpr int kTStride = 129;  // pass-2 transpose buffer row stride (floats)
 
@@ -102,6 +103,7 @@ __device__ float block_max(float v, float* red) {
 // Representative pass. PASS 1: A = Q^ (128 rep rows), B = K tile -> TMEM
 // lane = rep row r, column = key. PASS 2: A = K tile, B = Q^ -> lane = key,
 // column = rep row r. Both are M=N=K=128 bf16 UMMAs on K-major SW128 tiles.
+// 8 warps: warp w reads TMEM lane quarter (w % 4) and column half (w / 4).
 template <int PASS>
 __global__ void __launch_bounds__(kRepThreads, 1)
     rep_pass(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
@@ -116,6 +118,8 @@ __global__ void __launch_bounds__(kRepThreads, 1)
   float* T = reinterpret_cast<float*>(sbase + sizeof(RepSmem));  // PASS 2 only
 
   const int tid = threadIdx.x;
+  const int wq = warp_id() & 3, half = warp_id() >> 2;
+  const int lane_row = wq * 32 + lane_id();  // TMEM lane of this thread
   const int chunk = blockIdx.x, h = blockIdx.y;
   const int g = h / (H / G);
   const int t0 = chunk * kChunkTiles;
@@ -131,7 +135,7 @@ __global__ void __launch_bounds__(kRepThreads, 1)
     for (int b = 0; b < 2; ++b) mbar_init(&sm.mma_done[b], 1);
     mbar_fence_init();
   }
-  if (PASS == 2) {
+  if (PASS == 2 && tid < 128) {
     sm.m_row[tid] = m_row[h * 128 + tid];
     sm.il_row[tid] = il_row[h * 128 + tid];
   }
@@ -166,78 +170,90 @@ __global__ void __launch_bounds__(kRepThreads, 1)
     issue_mma(0);
   }
 
-  float m_loc = -INFINITY, l_loc = 0.f;  // PASS 1 running row stats (log2 domain)
+  float m_loc = -INFINITY, l_loc = 0.f;  // PASS 1 running row stats of this column half (log2)
 
   for (int t = 0; t < ntile; ++t) {
     if (tid == 0 && t + 1 < ntile) issue_mma(t + 1);
     const int b = t & 1;
     const int tile = t0 + t;
+    const bool last = (tile == nb - 1);
     mbar_wait(&sm.mma_done[b], (t >> 1) & 1);
     tc_fence_after();
 
-    uint32_t v[128];
-    const uint32_t lane_base = (uint32_t)(warp_id() * 32);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld32(tmem_addr(tbase + b * 128, lane_base, c * 32), v + c * 32);
+    uint32_t v[64];
+    const uint32_t ta = tmem_addr(tbase + b * 128, wq * 32, half * 64);
+    tmem_ld32(ta, v);
+    tmem_ld32(ta + 32, v + 32);
     tmem_wait_ld();
 
     if (PASS == 1) {
       // lane = rep row r; key j = tile*128 + c visible iff j <= p_r = n-128+r
-      const int r = tid;
-      const bool last = (tile == nb - 1);
-      float mx = -INFINITY;
+      const int r = lane_row;
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
+      for (int c = 0; c < 64; ++c) {
         float x = __uint_as_float(v[c]) * scale_log2;
-        if (last && c > r) x = -INFINITY;
+        if (last && half * 64 + c > r) x = -INFINITY;
         v[c] = __float_as_uint(x);
-        mx = fmaxf(mx, x);
+        mx4[c & 3] = fmaxf(mx4[c & 3], x);
       }
-      const float m_new = fmaxf(m_loc, mx);
-      float sum = 0.f;
+      const float m_new = fmaxf(m_loc, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
+      // a column half can be fully masked (last tile, rows < 64): keep it at -inf, sum 0
+      const float m_safe = (m_new == -INFINITY) ? 0.f : m_new;
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < 128; ++c) sum += exp2f(__uint_as_float(v[c]) - m_new);
-      l_loc = l_loc * exp2f(m_loc - m_new) + sum;
+      for (int c = 0; c < 64; ++c) s4[c & 3] += fast_exp2(__uint_as_float(v[c]) - m_safe);
+      l_loc = l_loc * fast_exp2(m_loc - m_safe) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
       m_loc = m_new;
       if (do_kbar) {
-        // avg-pooled key of this block, dimension d = tid (fixed row order)
+        // avg-pooled key of this block: dimension d = tid % 128, rows of this half
         const uint8_t* kt = sm.kst[t % kStages];
-        float acc = 0.f;
-        for (int row = 0; row < 128; ++row)
-          acc += bf16_to_f32(*reinterpret_cast<const uint16_t*>(kt + sw128_offset(row, tid)));
-        k_bar[((size_t)g * nb + tile) * 128 + tid] = acc * (1.0f / 128.0f);
+        const int d = tid & 127, r0 = (tid >> 7) * 64;
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+        for (int row = 0; row < 64; row += 2) {
+          a0 += bf16_to_f32(*reinterpret_cast<const uint16_t*>(kt + sw128_offset(r0 + row, d)));
+          a1 += bf16_to_f32(*reinterpret_cast<const uint16_t*>(kt + sw128_offset(r0 + row + 1, d)));
+        }
+        sm.red[tid] = a0 + a1;
+        __syncthreads();
+        if (tid < 128)
+          k_bar[((size_t)g * nb + tile) * 128 + tid] = (sm.red[tid] + sm.red[tid + 128]) * (1.0f / 128.0f);
       }
     } else {
-      // lane = key j_local, column = rep row r
-      const int jl = tid;
+      // lane = key j_local, columns = rep rows r = half*64 .. half*64+63
+      const int jl = lane_row;
       const int j = tile * 128 + jl;
-      const bool last = (tile == nb - 1);
-      float colsum = 0.f;
-      float* Trow = T + jl * kTStride;
+      float cs[4] = {0.f, 0.f, 0.f, 0.f};
+      float* Trow = T + jl * kTStride + half * 64;
 #pragma unroll
-      for (int r = 0; r < 128; ++r) {
-        float x = __uint_as_float(v[r]) * scale_log2;
-        float p = exp2f(x - sm.m_row[r]) * sm.il_row[r];
+      for (int c = 0; c < 64; ++c) {
+        const int r = half * 64 + c;
+        float p = fast_exp2(fmaf(__uint_as_float(v[c]), scale_log2, -sm.m_row[r])) * sm.il_row[r];
         if (last && jl > r) p = 0.f;
-        colsum += p;
-        Trow[r] = p;
+        cs[c & 3] += p;
+        Trow[c] = p;
       }
-      a_v[(size_t)h * n + j] = colsum * (1.0f / 128.0f);
+      sm.red[half * 128 + jl] = (cs[0] + cs[1]) + (cs[2] + cs[3]);
       __syncthreads();
-      // slash partials: diagonal delta = r - jl in [-127, 127]
+      if (tid < 128) a_v[(size_t)h * n + tile * 128 + tid] = (sm.red[tid] + sm.red[128 + tid]) * (1.0f / 128.0f);
+      (void)j;
+      // slash partials: diagonal delta = r - jl in [-127, 127], one per thread;
       // offset o = p_r - j = (n - 128 - tile*128) + delta
-      float* out = as_part + ((size_t)h * nb + tile) * 256;
-      {
-        const int d1 = tid - 127;  // -127 .. 0
-        float s = 0.f;
-        for (int q = max(0, -d1); q < 128 - max(0, d1); ++q) s += T[q * kTStride + q + d1];
-        out[d1 + 127] = s;
-      }
-      if (tid < 127) {
-        const int d2 = tid + 1;  // 1 .. 127
-        float s = 0.f;
-        for (int q = 0; q < 128 - d2; ++q) s += T[q * kTStride + q + d2];
-        out[d2 + 127] = s;
+      if (tid < 255) {
+        const int dl = tid - 127;
+        const int q0 = max(0, -dl), q1 = 128 - max(0, dl);
+        const float* tp = T + q0 * (kTStride + 1) + dl;
+        float s0 = 0.f, s1 = 0.f;
+        int q = q0;
+#pragma unroll 4
+        for (; q + 1 < q1; q += 2) {
+          s0 += tp[0];
+          s1 += tp[kTStride + 1];
+          tp += 2 * (kTStride + 1);
+        }
+        if (q < q1) s0 += tp[0];
+        as_part[((size_t)h * nb + tile) * 256 + dl + 127] = s0 + s1;
       }
     }
     tc_fence_before();
@@ -250,8 +266,17 @@ __global__ void __launch_bounds__(kRepThreads, 1)
   }
 
   if (PASS == 1) {
-    m_part[((size_t)h * nchunks + chunk) * 128 + tid] = m_loc;
-    l_part[((size_t)h * nchunks + chunk) * 128 + tid] = l_loc;
+    // combine the two column halves of each row
+    sm.red[tid] = m_loc;
+    sm.red[256 + tid] = l_loc;
+    __syncthreads();
+    if (tid < 128) {
+      const float m0 = sm.red[tid], m1 = sm.red[tid + 128];
+      const float m = fmaxf(m0, m1);
+      const float l = sm.red[256 + tid] * fast_exp2(m0 - m) + sm.red[256 + tid + 128] * fast_exp2(m1 - m);
+      m_part[((size_t)h * nchunks + chunk) * 128 + tid] = m;
+      l_part[((size_t)h * nchunks + chunk) * 128 + tid] = l;
+    }
   }
   tc_fence_before();
   __syncthreads();

@@ -62,30 +62,60 @@ __device__ uint64_t block_scan_u64(uint64_t v, uint64_t* wsum, uint64_t* total) 
   return v + add;
 }
 
+constexpr int kCl = 4;  // CTAs (one cluster) per top-mass segment
+
+// distributed shared memory helpers (thread block cluster)
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t cl_ld32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long cl_ld64(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+
 struct TopSmem {
-  uint32_t cnt[2048];
+  uint32_t cnt[2048];             // this CTA's histogram of its slice
   unsigned long long mass[2048];
+  uint32_t gcnt[2048];            // cluster-wide histogram (sum over the kCl CTAs)
+  unsigned long long gmass[2048];
   uint64_t wsum[32];
-  // selection state
-  uint32_t prefix;
   uint32_t found_bin;
   unsigned long long above_mass, above_cnt;
-  unsigned long long bin_mass, bin_cnt;
-  unsigned long long red[32];
+  unsigned long long slice_gt, slice_eq;  // compaction counts of this CTA's slice
 };
 
-// topmass(x, gamma) of one segment; see file header.
-__global__ void __launch_bounds__(kSelThreads, 1)
+// topmass(x, gamma) of one segment by a cluster of kCl CTAs; see file header.
+// CTA c of the cluster owns the index slice [c*S, (c+1)*S), S = ceil(L / kCl).
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads, 1)
     topmass_kernel(const float* __restrict__ a_v, const float* __restrict__ a_s,
                    const float* __restrict__ A_bar, const int32_t* __restrict__ pattern, int n,
                    long long tri, float gamma, int32_t* __restrict__ sel_v,
                    int32_t* __restrict__ sel_s, int32_t* __restrict__ sel_qa,
                    int32_t* __restrict__ sel_count, unsigned long long* __restrict__ sel_mass) {
-  __shared__ TopSmem sm;
-  const int seg = blockIdx.x, h = blockIdx.y;
+  extern __shared__ __align__(16) uint8_t top_raw[];
+  TopSmem& sm = *reinterpret_cast<TopSmem*>(top_raw);
+  const int seg = blockIdx.x / kCl, h = blockIdx.y;
+  const uint32_t crank = cl_rank();
+  const int tid = threadIdx.x;
   const int pat = pattern[h];
-  if ((pat == 1) != (seg == 2)) {
-    if (threadIdx.x == 0) {
+  if ((pat == 1) != (seg == 2)) {  // whole cluster leaves together
+    if (tid == 0 && crank == 0) {
       sel_count[h * 4 + seg] = 0;
       sel_mass[h * 4 + seg] = 0;
     }
@@ -107,30 +137,11 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     out = sel_qa + (size_t)h * tri;
     L = tri;
   }
-  const int tid = threadIdx.x;
+  const long long S = (L + kCl - 1) / kCl;
+  const long long lo = min(L, (long long)crank * S), hi = min(L, lo + S);
 
-  // ---- total mass T (fixed point, exact)
-  unsigned long long t_loc = 0;
-  for (long long i = tid; i < L; i += kSelThreads) t_loc += fixp(x[i]);
-  for (int o = 16; o > 0; o >>= 1) t_loc += __shfl_xor_sync(0xffffffffu, t_loc, o);
-  if (lane_id() == 0) sm.red[warp_id()] = t_loc;
-  __syncthreads();
-  unsigned long long T = 0;
-  for (int w = 0; w < 32; ++w) T += sm.red[w];
-
-  if (gamma >= 1.0f) {  // A7: gamma >= 1 selects everything
-    for (long long i = tid; i < L; i += kSelThreads) out[i] = (int32_t)i;
-    if (tid == 0) {
-      sel_count[h * 4 + seg] = (int32_t)L;
-      sel_mass[h * 4 + seg] = T;
-    }
-    return;
-  }
-  // K = min{k : C_k >= gamma T}  (A6, A7); G == 0 -> K = 1 (count mode)
-  const unsigned long long G = (unsigned long long)ceil((double)gamma * (double)T);
-  const bool count_mode = (G == 0);
-  unsigned long long rem = count_mode ? 1ull : G;
-
+  unsigned long long T = 0, G = 0, rem = 0;
+  bool count_mode = false;
   uint32_t prefix = 0, pmask = 0;
   unsigned long long above_mass_tot = 0, above_cnt_tot = 0;
   const int shifts[3] = {21, 10, 0};
@@ -144,20 +155,19 @@ __global__ void __launch_bounds__(kSelThreads, 1)
       sm.mass[b] = 0;
     }
     __syncthreads();
-    for (long long base = 0; base < L; base += kSelThreads) {
+    // local histogram of the slice (warp-aggregated smem atomics)
+    for (long long base = lo; base < hi; base += kSelThreads) {
       const long long i = base + tid;
-      const bool valid = i < L;
-      uint32_t key = valid ? __float_as_uint(x[i]) : 0xffffffffu;
+      const bool valid = i < hi;
+      const uint32_t key = valid ? __float_as_uint(x[i]) : 0xffffffffu;
       const bool match = valid && ((key & pmask) == prefix);
       const uint32_t digit = match ? ((key >> sh) & dmask) : 0xffffffffu;
       const uint32_t grp = __match_any_sync(0xffffffffu, digit);
       if (match) {
         const uint64_t f = fixp(__uint_as_float(key));
-        const uint32_t c0 = (uint32_t)(f & 0xFFFFF), c1 = (uint32_t)((f >> 20) & 0xFFFFF),
-                       c2 = (uint32_t)(f >> 40);
-        const uint32_t s0 = __reduce_add_sync(grp, c0);
-        const uint32_t s1 = __reduce_add_sync(grp, c1);
-        const uint32_t s2 = __reduce_add_sync(grp, c2);
+        const uint32_t s0 = __reduce_add_sync(grp, (uint32_t)(f & 0xFFFFF));
+        const uint32_t s1 = __reduce_add_sync(grp, (uint32_t)((f >> 20) & 0xFFFFF));
+        const uint32_t s2 = __reduce_add_sync(grp, (uint32_t)(f >> 40));
         if ((__ffs(grp) - 1) == (int)lane_id()) {
           atomicAdd(&sm.cnt[digit], (uint32_t)__popc(grp));
           atomicAdd(&sm.mass[digit], ((unsigned long long)s2 << 40) +
@@ -165,27 +175,55 @@ __global__ void __launch_bounds__(kSelThreads, 1)
         }
       }
     }
-    __syncthreads();
+    cl_sync();  // every CTA's local histogram is complete
+    for (int b = tid; b < nbins; b += kSelThreads) {
+      uint32_t c = 0;
+      unsigned long long m = 0;
+      for (uint32_t r = 0; r < kCl; ++r) {  // fixed order; integer sums are exact anyway
+        c += cl_ld32(cl_map(&sm.cnt[b], r));
+        m += cl_ld64(cl_map(&sm.mass[b], r));
+      }
+      sm.gcnt[b] = c;
+      sm.gmass[b] = m;
+    }
+    cl_sync();  // remote reads done before anyone clears its histogram
+    if (pass == 0) {
+      // total mass T from the first-digit histogram (exact, fixed point)
+      unsigned long long tl = 0;
+      for (int b = tid; b < nbins; b += kSelThreads) tl += sm.gmass[b];
+      uint64_t tot;
+      block_scan_u64(tl, sm.wsum, &tot);
+      T = tot;
+      if (gamma >= 1.0f) {  // A7: gamma >= 1 selects everything
+        for (long long i = lo + tid; i < hi; i += kSelThreads) out[i] = (int32_t)i;
+        if (tid == 0 && crank == 0) {
+          sel_count[h * 4 + seg] = (int32_t)L;
+          sel_mass[h * 4 + seg] = T;
+        }
+        cl_sync();
+        return;
+      }
+      // K = min{k : C_k >= gamma T}  (A6, A7); G == 0 -> K = 1 (count mode)
+      G = (unsigned long long)ceil((double)gamma * (double)T);
+      count_mode = (G == 0);
+      rem = count_mode ? 1ull : G;
+    }
     // descending-digit scan: thread t owns digits nbins-1-2t and nbins-2-2t
     const int d0 = nbins - 1 - 2 * tid, d1 = d0 - 1;
     uint64_t m0 = 0, m1 = 0, k0 = 0, k1 = 0;
     if (d0 >= 0) {
-      m0 = sm.mass[d0];
-      k0 = sm.cnt[d0];
+      m0 = sm.gmass[d0];
+      k0 = sm.gcnt[d0];
     }
     if (d1 >= 0) {
-      m1 = sm.mass[d1];
-      k1 = sm.cnt[d1];
+      m1 = sm.gmass[d1];
+      k1 = sm.gcnt[d1];
     }
     uint64_t tot;
     const uint64_t key_m = count_mode ? (k0 + k1) : (m0 + m1);
-    const uint64_t incl = block_scan_u64(key_m, sm.wsum, &tot);
-    const uint64_t excl = incl - key_m;
-    // second scan for the other quantity (mass when counting, count when massing)
+    const uint64_t excl = block_scan_u64(key_m, sm.wsum, &tot) - key_m;
     const uint64_t other = count_mode ? (m0 + m1) : (k0 + k1);
-    const uint64_t incl_o = block_scan_u64(other, sm.wsum, &tot);
-    const uint64_t excl_o = incl_o - other;
-    // crossing: above < rem <= above + bin
+    const uint64_t excl_o = block_scan_u64(other, sm.wsum, &tot) - other;
     {
       const uint64_t q0 = count_mode ? k0 : m0, q1 = count_mode ? k1 : m1;
       const uint64_t o0 = count_mode ? m0 : k0;
@@ -193,19 +231,14 @@ __global__ void __launch_bounds__(kSelThreads, 1)
         sm.found_bin = d0;
         sm.above_mass = count_mode ? excl_o : excl;
         sm.above_cnt = count_mode ? excl : excl_o;
-        sm.bin_mass = m0;
-        sm.bin_cnt = k0;
       } else if (d1 >= 0 && excl + q0 < rem && rem <= excl + q0 + q1) {
         sm.found_bin = d1;
         sm.above_mass = count_mode ? excl_o + o0 : excl + q0;
         sm.above_cnt = count_mode ? excl + q0 : excl_o + o0;
-        sm.bin_mass = m1;
-        sm.bin_cnt = k1;
       }
     }
     __syncthreads();
-    const uint32_t B = sm.found_bin;
-    prefix |= B << sh;
+    prefix |= sm.found_bin << sh;
     pmask |= dmask << sh;
     above_mass_tot += sm.above_mass;
     above_cnt_tot += sm.above_cnt;
@@ -218,30 +251,49 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   const uint64_t t_take = count_mode ? rem : (rem + f_lam - 1) / f_lam;
   const uint64_t K = above_cnt_tot + t_take;
 
-  // ordered compaction: selected = key > lam, or key == lam among the first t_take ties
+  // slice counts (> lambda, == lambda), exchanged across the cluster for the offsets
+  {
+    unsigned long long gt = 0, eq = 0;
+    for (long long i = lo + tid; i < hi; i += kSelThreads) {
+      const uint32_t key = __float_as_uint(x[i]);
+      gt += key > lam;
+      eq += key == lam;
+    }
+    uint64_t tot;
+    block_scan_u64((eq << 32) | gt, sm.wsum, &tot);
+    if (tid == 0) {
+      sm.slice_gt = tot & 0xffffffffu;
+      sm.slice_eq = tot >> 32;
+    }
+  }
+  cl_sync();
   uint64_t gt_run = 0, eq_run = 0;
-  for (long long base = 0; base < L; base += (long long)kSelThreads * kItems) {
+  for (uint32_t r = 0; r < crank; ++r) {
+    gt_run += cl_ld64(cl_map(&sm.slice_gt, r));
+    eq_run += cl_ld64(cl_map(&sm.slice_eq, r));
+  }
+  // ordered compaction of this slice
+  for (long long base = lo; base < hi; base += (long long)kSelThreads * kItems) {
     const long long i0 = base + (long long)tid * kItems;
     uint32_t keys[kItems];
     uint32_t gt = 0, eq = 0;
 #pragma unroll
     for (int u = 0; u < kItems; ++u) {
       const long long i = i0 + u;
-      keys[u] = (i < L) ? __float_as_uint(x[i]) : 0u;
-      const bool valid = i < L;
+      const bool valid = i < hi;
+      keys[u] = valid ? __float_as_uint(x[i]) : 0u;
       gt += (valid && keys[u] > lam);
       eq += (valid && keys[u] == lam);
     }
     uint64_t tot;
     const uint64_t packed = ((uint64_t)eq << 32) | gt;
-    const uint64_t incl = block_scan_u64(packed, sm.wsum, &tot);
-    const uint64_t excl = incl - packed;
+    const uint64_t excl = block_scan_u64(packed, sm.wsum, &tot) - packed;
     uint64_t eq_pre = eq_run + (excl >> 32);
     uint64_t pos = gt_run + (excl & 0xffffffffu) + min(t_take, eq_pre);
 #pragma unroll
     for (int u = 0; u < kItems; ++u) {
       const long long i = i0 + u;
-      if (i >= L) break;
+      if (i >= hi) break;
       bool take = keys[u] > lam;
       if (keys[u] == lam) {
         take = eq_pre < t_take;
@@ -252,10 +304,11 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     gt_run += tot & 0xffffffffu;
     eq_run += tot >> 32;
   }
-  if (tid == 0) {
+  if (tid == 0 && crank == 0) {
     sel_count[h * 4 + seg] = (int32_t)K;
     sel_mass[h * 4 + seg] = above_mass_tot + t_take * f_lam;
   }
+  cl_sync();  // keep this CTA's shared memory alive until the cluster is done
 }
 
 // vertical-block and slash-diagonal bitmaps of VS heads (A10, reading R1)
@@ -448,7 +501,13 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
                           int32_t* row_ptr, int32_t* col_idx, fp_select_stats* stats,
                           cudaStream_t st) {
   const int32_t* pat = wsp<int32_t>(ws, L.pattern);
-  topmass_kernel<<<dim3(3, s.H), kSelThreads, 0, st>>>(
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(topmass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TopSmem));
+    attr_done = true;
+  }
+  topmass_kernel<<<dim3(3 * kCl, s.H), kSelThreads, sizeof(TopSmem), st>>>(
       wsp<float>(ws, L.a_v), wsp<float>(ws, L.a_s), wsp<float>(ws, L.A_bar), pat, s.n, s.tri, gamma,
       wsp<int32_t>(ws, L.sel_v), wsp<int32_t>(ws, L.sel_s), wsp<int32_t>(ws, L.sel_qa),
       wsp<int32_t>(ws, L.sel_count), wsp<unsigned long long>(ws, L.sel_mass));
