@@ -1,0 +1,116 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration
+bench.py times (whole layer through the binding), checked against the
+float64 oracle on sampled heads and sampled query blocks (the oracle cannot
+do a whole 128k layer in seconds): stage-wise plan / selection / CSR parity
+for the sampled heads, and attention outputs on sampled q-blocks (always
+including qb = 0, 1, nb/2, nb-1) within max-abs 2e-2 / mean-abs 2e-3.
+Whole-layer properties that hold at any size are checked for every head:
+CSR rows sorted, forced blocks present, budget floor, pattern = planted type.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth import gen
+from synth.configs import C2, C3, C4, Workload
+from tests import parity
+from tests.test_gpu_parity import MAX_ABS, MEAN_ABS
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def fp():
+    import paper_2502_20766_b200 as m
+    m.load_library()
+    return m
+
+
+def _sample_heads(w, k=4):
+    g = w.heads // w.kv_heads
+    vs = [h for h in range(w.heads) if h % g != g - 1]
+    qa = [h for h in range(w.heads) if h % g == g - 1]
+    rng = np.random.default_rng(w.seed)
+    pick = list(rng.choice(vs, k // 2, replace=False)) + list(rng.choice(qa, k - k // 2, replace=False))
+    return sorted(int(h) for h in pick)
+
+
+def _run(fp, w, heads_checked):
+    q, k, v = gen.make_layer_bits(w)
+    res = parity.run_gpu(fp, w, q, k, v)
+    nb = w.seq_len // 128
+    m = -(-w.min_budget // 128) if w.min_budget else 0
+    # whole-layer properties (every head)
+    for h in range(w.heads):
+        rp, ci = res["row_ptr"][h], res["col_idx"][h]
+        assert parity.csr_rows_sorted(rp, ci, nb), h
+        assert np.all(np.diff(rp) >= np.minimum(np.arange(nb) + 1, max(m, 1))), h
+        want = oracle.QA if gen.is_qa_type(h, w.heads, w.kv_heads) else oracle.VS
+        assert res["pattern"][h] == want, (h, res["jsd"][h])
+    rng = np.random.default_rng(7)
+    qblocks = sorted({0, 1, nb // 2, nb - 1, *rng.integers(0, nb, 4).tolist()})
+    worst = (0.0, 0.0)
+    for h in heads_checked:
+        g = h * w.kv_heads // w.heads
+        Q = gen.bits_to_f64(q[h])
+        K = gen.bits_to_f64(k[g])
+        V = gen.bits_to_f64(v[g])
+        p = oracle.plan_head(Q, K, 128, w.tau)
+        assert res["pattern"][h] == p["pattern"]
+        assert abs(res["jsd"][h] - p["D"]) <= 1e-4, (h, res["jsd"][h], p["D"])
+        for key in ("a_v", "a_s", "a_hat", "a_bar"):
+            rel, small = parity.rel_close(res["dbg"][key][h], p[key], 1e-4, 1e-6)
+            assert rel <= 1e-4 and small <= 1e-7, (h, key, rel, small)
+        dbg = res["dbg"]
+        cnt = dbg["sel_count"][h]
+        if p["pattern"] == oracle.VS:
+            for seg, key in ((0, "a_v"), (1, "a_s")):
+                sel = dbg["sel_v" if seg == 0 else "sel_s"][h, : cnt[seg]]
+                mi, eo, bd, _ = parity.classify(dbg[key][h].astype(np.float64), w.gamma, sel,
+                                                parity.STAGE_DELTA, 0.0)
+                assert mi == 0 and eo == 0 and bd == 0, (h, key)
+                # end-to-end vs the oracle's own scores: borderline rule
+                mi, eo, bd, nbd = parity.classify(p[key], w.gamma, sel)
+                assert mi == 0 and eo == 0, (h, key, mi, eo, bd, nbd)
+        else:
+            tri = nb * (nb + 1) // 2
+            sel = dbg["sel_qa"][h, : cnt[2]]
+            mi, eo, bd, _ = parity.classify(dbg["A_bar"][h, :tri].astype(np.float64), w.gamma, sel,
+                                            parity.STAGE_DELTA, 0.0)
+            assert mi == 0 and eo == 0 and bd == 0, h
+            vals, _, _ = oracle.qa_flat(oracle.qa_pooled_map(Q, K, 128))
+            mi, eo, bd, nbd = parity.classify(vals, w.gamma, sel)
+            assert mi == 0 and eo == 0, (h, mi, eo, bd, nbd)
+        M0, M = parity.stagewise_mask(res["pattern"][h], dbg, h, w.seq_len, w.gamma, w.min_budget)
+        Mg = parity.csr_mask(res["row_ptr"][h], res["col_idx"][h], nb)
+        assert np.array_equal(Mg, M), h
+        ref = oracle.sparse_attention(Q, K, V, Mg, 128, qblocks)
+        rows = ~np.isnan(ref[:, 0])
+        d = np.abs(res["out"][h][rows] - ref[rows])
+        assert d.max() <= MAX_ABS and d.mean() <= MEAN_ABS, (h, d.max(), d.mean())
+        worst = (max(worst[0], float(d.max())), max(worst[1], float(d.mean())))
+    return res, worst
+
+
+def test_c2_llama_32k(fp):
+    _run(fp, C2, _sample_heads(C2, 4))
+
+
+def test_c3_llama_128k(fp):
+    _run(fp, C3, _sample_heads(C3, 4))
+
+
+def test_c3_llama_128k_gamma09(fp):
+    w = C3.with_(gamma=0.9)
+    _run(fp, w, _sample_heads(w, 2))
+
+
+def test_c4_glm_128k_min_budget(fp):
+    res, _ = _run(fp, C4, _sample_heads(C4, 2))
+    assert sum(s["budget_added"] for s in res["stats"]) > 0
+
+
+def test_qwen_28_4_uneven_groups(fp):
+    # Qwen2-7B-like layout (g = 7), reduced length
+    w = Workload("qwen-8k", 28, 4, 8192, 0.9, 0.1, 0, 105)
+    _run(fp, w, _sample_heads(w, 2))

@@ -1,0 +1,131 @@
+"""Configuration sweeps of BASELINE.json configs[3] and configs[4] (1 GPU).
+
+    python tools/sweep.py c4            # GLM-4-9B-like 32/2 at 128k: gamma sweep, min budget 1024 and 0
+    python tools/sweep.py c5            # Qwen2-7B 28/4 and Yi-9B 32/4: 4k..128k, tau sweep
+    python tools/sweep.py c3            # Llama 32/8 128k at gamma 0.9 and 0.95
+
+One JSON line per point: layer latency (plan+select+attn) and dense latency
+(same library, same GPU) from CUDA events, speedup, tokens/s, density,
+pattern counts, attention TFLOP/s on computed blocks. Inputs are generated
+once per (layout, n) and reused across gamma / tau.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from synth import configs as C  # noqa: E402
+from synth import gen  # noqa: E402
+
+
+def useful_flops(nnz, nb):
+    return sum(4 * 128 * (128 * 128 * (int(x) - nb) + nb * 128 * 129 // 2) for x in nnz)
+
+
+def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flush=None):
+    st = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def timed(fn, n_steps, n_warm):
+        for _ in range(n_warm):
+            fn()
+        torch.cuda.synchronize()
+        tot = []
+        for _ in range(n_steps):
+            if flush is not None:
+                flush.zero_()
+            a, b = ev(), ev()
+            a.record(st)
+            fn()
+            b.record(st)
+            tot.append((a, b))
+        torch.cuda.synchronize()
+        return float(np.mean([a.elapsed_time(b) for a, b in tot]))
+
+    def layer():
+        fpl.plan(q, k, w.tau)
+        fpl.select(w.gamma, w.min_budget, with_stats=False)
+        fpl.attn(q, k, v, out)
+
+    ms = timed(layer, steps, warmup)
+    fpl.plan(q, k, w.tau)
+    fpl.select(w.gamma, w.min_budget)
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    a.record(st)
+    fpl.attn(q, k, v, out)
+    b.record(st)
+    torch.cuda.synchronize()
+    attn_ms = a.elapsed_time(b)
+    stats = fpl.stats()
+    nb = w.seq_len // 128
+    nnz = [s_["nnz_blocks"] for s_ in stats]
+    pats = [s_["pattern"] for s_ in stats]
+    dms = timed(lambda: fpl.dense(q, k, v, out), max(2, steps // 2), 1) if dense else None
+    return {
+        "workload": w.name, "heads": w.heads, "kv_heads": w.kv_heads, "seq_len": w.seq_len,
+        "gamma": w.gamma, "tau": w.tau, "min_budget": w.min_budget,
+        "layer_ms": ms, "tokens_per_s": w.seq_len / (ms / 1e3), "attn_ms": attn_ms,
+        "dense_ms": dms, "speedup_vs_dense": (dms / ms) if dms else None,
+        "density": float(np.sum(nnz)) / (len(nnz) * nb * (nb + 1) / 2),
+        "qa_heads": int(np.sum(pats)), "vs_heads": int(len(pats) - np.sum(pats)),
+        "budget_added": int(sum(s_["budget_added"] for s_ in stats)),
+        "attn_tflops_useful": useful_flops(nnz, nb) / (attn_ms / 1e3) / 1e12,
+        "dense_tflops": (w.heads * 4 * 128 * w.seq_len * (w.seq_len + 1) / 2) / (dms / 1e3) / 1e12
+        if dms else None,
+    }
+
+
+def points(which):
+    if which == "c3":
+        for g in (0.9, 0.95):
+            yield C.C3.with_(gamma=g), None
+    elif which == "c4":
+        for mb in (1024, 0):
+            for g in C.C4_GAMMAS:
+                yield C.C4.with_(gamma=g, min_budget=mb), None
+    elif which == "c5":
+        for base in (C.C5_QWEN, C.C5_YI):
+            for n in C.C5_LENGTHS:
+                for t in C.C5_TAUS:
+                    yield base.with_(seq_len=n, tau=t, name=f"{base.name}-{n // 1024}k"), None
+
+
+def main():
+    import torch
+    import paper_2502_20766_b200 as fp
+    which = sys.argv[1]
+    out_path = sys.argv[2] if len(sys.argv) > 2 else None
+    fp.load_library()
+    cache = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    f = open(out_path, "a") if out_path else None
+    for w, _ in points(which):
+        key = (w.heads, w.kv_heads, w.seq_len, w.seed)
+        if key not in cache:
+            cache.clear()
+            torch.cuda.empty_cache()
+            t = time.time()
+            qb, kb, vb = gen.make_layer_bits(w)
+            q, k, v = (torch.from_numpy(x).view(torch.bfloat16).cuda() for x in (qb, kb, vb))
+            del qb, kb, vb
+            fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len)
+            cache[key] = (q, k, v, fpl, torch.empty_like(q))
+            print(f"# generated {key} in {time.time() - t:.1f}s", file=sys.stderr, flush=True)
+        q, k, v, fpl, out = cache[key]
+        steps = 5 if w.seq_len >= 65536 else 10
+        r = measure(fp, torch, w, q, k, v, fpl, out, steps=steps, warmup=2, flush=flush)
+        line = json.dumps(r)
+        print(line, flush=True)
+        if f:
+            f.write(line + "\n")
+            f.flush()
+
+
+if __name__ == "__main__":
+    main()
