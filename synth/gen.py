@@ -51,11 +51,12 @@ GAINS = dict(
     local=7.5,        # + lambda_n, peak of the two Dirichlet local kernels
     period1=2048.0,
     period2=3000.0,
-    warm=1.5,         # block warmth logit bias = warm * z_kb, z ~ N(0, 1)
+    warm=1.0,         # block warmth logit bias = warm * z_kb, z ~ N(0, 1)
     warm_frac=0.15,   # warmest fraction of blocks carry no heavy hitter
     cluster=8.0,      # + lambda_n, Query-Aware cluster match
     qa_sink=2.0,      # weak sink of Query-Aware heads (no lambda_n)
     head_jitter=0.05,
+    lam_coef=0.6,     # boosts grow by lam_coef * ln(n / 2048)
 )
 
 ROLE_Q, ROLE_K, ROLE_V, ROLE_KVMETA, ROLE_QMETA = 1, 2, 3, 4, 5
@@ -100,8 +101,8 @@ def _rng(seed, H, G, n, role, idx):
     return np.random.default_rng([seed, H, G, n, role, idx])
 
 
-def _lam(n):
-    return math.log(max(n, 2048) / 2048.0)
+def _lam(n, gains=GAINS):
+    return gains["lam_coef"] * math.log(max(n, 2048) / 2048.0)
 
 
 def kv_meta(seed, H, G, n, g, gains=GAINS):
@@ -139,7 +140,6 @@ def _dirichlet(pos, amp, period):
 
 
 def make_k(seed, H, G, n, g, gains=GAINS):
-    lam = _lam(n)
     meta = kv_meta(seed, H, G, n, g, gains)
     r = _rng(seed, H, G, n, ROLE_K, g)
     K = np.zeros((n, D), np.float32)
@@ -163,7 +163,7 @@ def make_v(seed, H, G, n, g):
 
 
 def make_q(seed, H, G, n, h, gains=GAINS):
-    lam = _lam(n)
+    lam = _lam(n, gains)
     r = _rng(seed, H, G, n, ROLE_Q, h)
     rm = _rng(seed, H, G, n, ROLE_QMETA, h)
     Q = np.zeros((n, D), np.float32)
