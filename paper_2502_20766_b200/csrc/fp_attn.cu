@@ -3,28 +3,25 @@
 // k-block) pairs with online softmax and GQA, on tcgen05 tensor cores.
 //
 // One CTA per (head, query block) work item, warp-specialised (384 threads;
-// registers rebalanced with setmaxnreg: 224 per softmax thread, 56 otherwise):
+// registers rebalanced with setmaxnreg: 200 per softmax thread, 56 otherwise):
 //   warp 8   K producer    Q tile once, then the K tiles of the row's key blocks
 //                          (indices from the CSR) into a 3-stage TMA ring
 //   warp 10  V producer    the V tiles into their own 3-stage ring
-//   warp 9   MMA issuer    S_i = Q K_i^T into TMEM buffer (i & 1), issued two
-//                          tiles ahead; O_(i&1) += P_i V_i with P_i read from
-//                          TMEM (tcgen05 "TS" form, A operand in tensor memory)
-//   warps 0-3 / 4-7        two softmax warpgroups that ping-pong over the key
-//                          tiles: warpgroup w owns tiles i = w, w+2, ..., its
-//                          S/P buffer, its O accumulator and its own running
-//                          (max, sum); one query row per thread. While one
-//                          warpgroup exponentiates, the tensor core works for
-//                          the other. The running max is lazy (O_w is rescaled
-//                          only when the max grows by more than 2^8); the two
-//                          partial softmaxes are merged once, in the epilogue.
-// TMEM (512 columns): S/P buffers 0 and 1 (128 each), O_0, O_1 (128 each).
-// Reusing an S/P buffer for S_(i+2) right after issuing PV_i relies on the
-// in-order execution of one thread's tcgen05.mma stream (WAR on the P
-// columns); a commit that follows S_i also guarantees PV_(i-2) is complete,
-// which is what makes the O_w rescale safe without another barrier.
-// A part of the exponentials runs on the FMA pipe (polynomial exp2) to keep
-// the MUFU pipe below the tensor-core time. The diagonal block gets the
+//   warp 9   MMA issuer    S_i = Q K_i^T into one of 3 TMEM S/P buffers, issued
+//                          two tiles ahead; O += P_i V_i with P_i read from TMEM
+//                          (tcgen05 "TS" form, A operand in tensor memory)
+//   warps 0-7 softmax      two warps per TMEM lane quarter, 16 query rows each;
+//                          TMEM is read with the 16x256b shape, so a row's 128
+//                          scores are spread over a quad of threads (32 each,
+//                          2 rows per thread): row max / sum need only quad
+//                          shuffles. Online softmax in the log2 domain with a
+//                          lazy running max (O is rescaled in TMEM only when the
+//                          max grows by more than 2^8); P (bf16) written back
+//                          over S (16x128b shape); final O / l -> global. An
+//                          optional polynomial exp2 on the FMA pipe (FP_EMU)
+//                          is compiled in but off by default (see below).
+// TMEM (512 columns): S/P buffers 0..2 (128 each), O (128).
+// The diagonal block (always the last of a row's sorted list) gets the
 // intra-block causal mask (j <= i) in a separate code path. The dense causal
 // kernel is the same template with the implicit list kb = 0..qb.
 // Work order is KV-group-major (the K/V of one group, 64 MiB at 128k, stays
@@ -46,12 +43,20 @@ namespace fp {
 namespace {
 
 constexpr int kAttnThreads = 384;      // 8 softmax warps, K producer (8), MMA (9), V producer (10), spare (11)
+// Measured on B200 (tools/attn_timing.py): under the 1 kW power cap the FMA-pipe
+// exp2 costs more than it saves (C3 128k attn: 35.4 ms at 0, 36.7 at 12, 37.5
+// at 20, 38.1 at 28 emulated values per thread), so the default is 0.
 #ifndef FP_EMU
-#define FP_EMU 32
+#define FP_EMU 0
 #endif
-constexpr int kEmu = FP_EMU;           // exponentials per row (of 128) done on the FMA pipe
+constexpr int kEmuK = FP_EMU / 4;      // of each thread's 16 column groups (4 values), this many
+                                       // are exponentiated on the FMA pipe
+constexpr int kSBuf = 3;               // S/P buffers in TMEM
 constexpr int kKV = 3;                 // K and V ring depths
-constexpr float kRescaleThresh = 8.0f; // lazy rescale: tolerate P up to 2^8
+#ifndef FP_RT
+#define FP_RT 8.0f
+#endif
+constexpr float kRescaleThresh = FP_RT; // lazy rescale: tolerate P up to 2^FP_RT
 
 struct AttnSmem {
   uint8_t q[kTileBytes];
@@ -60,14 +65,10 @@ struct AttnSmem {
   uint64_t q_full;
   uint64_t k_full[kKV], k_empty[kKV];
   uint64_t v_full[kKV], v_empty[kKV];
-  uint64_t s_full[2], p_full[2], pv_done[2];
+  uint64_t s_full[kSBuf], p_full[kSBuf], pv_done[kSBuf];
   uint32_t tmem_base;
-  float ml[2][2][128];  // epilogue exchange: (max, sum) per warpgroup and row
 };
 
-FP_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 FP_DEV float fmax3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
@@ -120,89 +121,89 @@ FP_DEV void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint3
 // One key tile of one softmax warpgroup: S row (128 fp32) from TMEM -> lazy
 // running max -> P = 2^(s - m) (bf16) written over the S columns. Returns the
 // row sum of P; updates m_used and sets alpha (scale for the previous O / l).
-#ifdef FP_TIMING
-#define FP_TARGS , bool timing_on, long long* tacc, long long& tlast
-#define FP_TPASS , timing_on, tacc, tlast
-#else
-#define FP_TARGS
-#define FP_TPASS
-#endif
+FP_DEV float quad_max(float v) {
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 1));
+  return fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 2));
+}
+FP_DEV float quad_sum(float v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v + __shfl_xor_sync(0xffffffffu, v, 2);
+}
+
+// One key tile for one softmax thread: rows R0 = c and R1 = c + 8 of its
+// 16-lane group (c = lane / 4), columns 8k + 2a, 8k + 2a + 1 (a = lane % 4).
+// v: the 64 scores (16x256b register order). Returns the partial row sums.
 template <bool DIAG>
-FP_DEV float softmax_tile(uint32_t tS, uint32_t tO, int r, float scale_log2, float& m_used,
-                          float& alpha, bool o_live FP_TARGS) {
-  float v[128];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, reinterpret_cast<uint32_t*>(v) + c * 32);
-  tmem_wait_ld();
-  FP_TMARK(1);
+FP_DEV void softmax_tile(float* v, int R0, int a, float scale_log2, float* m_used, float* alpha,
+                         float* rs) {
   if (DIAG) {
 #pragma unroll
-    for (int c = 0; c < 128; ++c)
-      if (c > r) v[c] = -INFINITY;
-  }
-  // row max on the raw logits (scale > 0): 8 independent 3-input-max chains
-  float acc[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) acc[u] = fmax3(v[u], v[u + 8], v[u + 16]);
-#pragma unroll
-  for (int c = 24; c < 120; c += 16)
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] = fmax3(acc[u], v[c + u], v[c + 8 + u]);
-#pragma unroll
-  for (int u = 0; u < 8; ++u) acc[u] = fmaxf(acc[u], v[120 + u]);
-  const float mx = fmax3(fmax3(acc[0], acc[1], acc[2]), fmax3(acc[3], acc[4], acc[5]),
-                         fmaxf(acc[6], acc[7])) * scale_log2;
-  // lazy running max: move it only when it grows by more than 2^kRescaleThresh
-  alpha = 1.0f;
-  const bool move = mx > m_used + kRescaleThresh;
-  if (move) {
-    alpha = exp2f(m_used - mx);  // 0 on the first tile
-    m_used = mx;
-  }
-  FP_TMARK(2);
-  if (o_live && __any_sync(0xffffffffu, move)) {
-    // O_w = sum over this warpgroup's earlier tiles; the PV that wrote it last
-    // completed before S of this tile (in-order tcgen05 stream + commit).
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t ov[32];
-      tmem_ld32(tO + c * 32, ov);
-      tmem_wait_ld();
-#pragma unroll
-      for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-      tmem_st32(tO + c * 32, ov);
+    for (int k = 0; k < 16; ++k) {
+      const int c0 = 8 * k + 2 * a;
+      if (c0 > R0) v[4 * k] = -INFINITY;
+      if (c0 + 1 > R0) v[4 * k + 1] = -INFINITY;
+      if (c0 > R0 + 8) v[4 * k + 2] = -INFINITY;
+      if (c0 + 1 > R0 + 8) v[4 * k + 3] = -INFINITY;
     }
   }
-  FP_TMARK(4);
-  const float neg = -m_used;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  // 4 chunks of 32 columns: scale, exponentiate (MUFU / FMA pipe), sum, pack, store P
+  // partial row maxima (raw logits; scale > 0), then across the quad
+  float p0 = fmax3(v[0], v[1], v[4]), p1 = fmax3(v[5], v[8], v[9]);
+  float q0 = fmax3(v[2], v[3], v[6]), q1 = fmax3(v[7], v[10], v[11]);
 #pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
-    float* x = v + ch * 32;
-#pragma unroll
-    for (int c = 0; c < 32; c += 2) ffma2(x[c], x[c + 1], x[c], x[c + 1], scale_log2, scale_log2, neg, neg);
-    constexpr int kEmuCh = kEmu / 4;  // emulated columns in each 32-column chunk
-#pragma unroll
-    for (int c = 0; c < 32 - kEmuCh; ++c) x[c] = fast_exp2(x[c]);
-#pragma unroll
-    for (int c = 32 - kEmuCh; c < 32; c += 2) exp2_emu2(x[c], x[c + 1], x[c], x[c + 1]);
-    if (DIAG) {
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (ch * 32 + c > r) x[c] = 0.f;
+  for (int k = 3; k < 16; k += 2) {
+    p0 = fmax3(p0, v[4 * k], v[4 * k + 1]);
+    q0 = fmax3(q0, v[4 * k + 2], v[4 * k + 3]);
+    if (k + 1 < 16) {
+      p1 = fmax3(p1, v[4 * k + 4], v[4 * k + 5]);
+      q1 = fmax3(q1, v[4 * k + 6], v[4 * k + 7]);
     }
-    uint32_t pk[16];
-#pragma unroll
-    for (int c = 0; c < 32; c += 4) {
-      fadd2(s0, s1, s0, s1, x[c], x[c + 1]);
-      fadd2(s2, s3, s2, s3, x[c + 2], x[c + 3]);
-      pk[c >> 1] = pack_bf16x2(x[c], x[c + 1]);
-      pk[(c >> 1) + 1] = pack_bf16x2(x[c + 2], x[c + 3]);
-    }
-    tmem_st16(tS + ch * 16, pk);  // P columns overwrite S columns already in registers
   }
-  return (s0 + s1) + (s2 + s3);
+  const float mx0 = quad_max(fmaxf(p0, p1)) * scale_log2;
+  const float mx1 = quad_max(fmaxf(q0, q1)) * scale_log2;
+  // lazy running max per row: move only when it grows by more than 2^kRescaleThresh
+  alpha[0] = 1.f;
+  alpha[1] = 1.f;
+  if (mx0 > m_used[0] + kRescaleThresh) {
+    alpha[0] = exp2f(m_used[0] - mx0);  // 0 on the first tile
+    m_used[0] = mx0;
+  }
+  if (mx1 > m_used[1] + kRescaleThresh) {
+    alpha[1] = exp2f(m_used[1] - mx1);
+    m_used[1] = mx1;
+  }
+  const float n0 = -m_used[0], n1 = -m_used[1];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    ffma2(v[4 * k], v[4 * k + 1], v[4 * k], v[4 * k + 1], scale_log2, scale_log2, n0, n0);
+    ffma2(v[4 * k + 2], v[4 * k + 3], v[4 * k + 2], v[4 * k + 3], scale_log2, scale_log2, n1, n1);
+  }
+#pragma unroll
+  for (int k = 0; k < 16 - kEmuK; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[4 * k + e] = fast_exp2(v[4 * k + e]);
+#pragma unroll
+  for (int k = 16 - kEmuK; k < 16; ++k) {
+    exp2_emu2(v[4 * k], v[4 * k + 1], v[4 * k], v[4 * k + 1]);
+    exp2_emu2(v[4 * k + 2], v[4 * k + 3], v[4 * k + 2], v[4 * k + 3]);
+  }
+  if (DIAG) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int c0 = 8 * k + 2 * a;
+      if (c0 > R0) v[4 * k] = 0.f;
+      if (c0 + 1 > R0) v[4 * k + 1] = 0.f;
+      if (c0 > R0 + 8) v[4 * k + 2] = 0.f;
+      if (c0 + 1 > R0 + 8) v[4 * k + 3] = 0.f;
+    }
+  }
+  float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    fadd2(s0, s1, s0, s1, v[4 * k], v[4 * k + 1]);
+    fadd2(t0, t1, t0, t1, v[4 * k + 2], v[4 * k + 3]);
+  }
+  rs[0] = s0 + s1;
+  rs[1] = t0 + t1;
 }
 
 template <bool DENSE>
@@ -250,9 +251,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kSBuf; ++b) {
       mbar_init(&sm.s_full[b], 1);
-      mbar_init(&sm.p_full[b], 128);
+      mbar_init(&sm.p_full[b], 256);
       mbar_init(&sm.pv_done[b], 1);
     }
     mbar_fence_init();
@@ -291,8 +292,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, true);
       const uint32_t qa = smem_u32(sm.q);
       auto issue_s = [&](int i) {
-        const int s = i % kKV, b = i & 1;
+        const int s = i % kKV, b = i % kSBuf;
         mbar_wait(&sm.k_full[s], (i / kKV) & 1);
+        // buffer b was last used by tile i-3: its P must have been consumed
+        if (i >= kSBuf) mbar_wait(&sm.pv_done[b], ((i - kSBuf) / kSBuf) & 1);
         tc_fence_after();
         const uint32_t ka = smem_u32(sm.k[s]);
 #pragma unroll
@@ -305,97 +308,106 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       issue_s(0);
       if (nk > 1) issue_s(1);
       for (int i = 0; i < nk; ++i) {
-        const int s = i % kKV, b = i & 1;
+        const int s = i % kKV, b = i % kSBuf;
         mbar_wait(&sm.v_full[s], (i / kKV) & 1);
-        mbar_wait(&sm.p_full[b], (i >> 1) & 1);
+        mbar_wait(&sm.p_full[b], (i / kSBuf) & 1);
         tc_fence_after();
         const uint32_t va = smem_u32(sm.v[s]);
-        const uint32_t tO = tbase + 256 + b * 128;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_bf16_ts(tO, tbase + b * 128 + kk * 8, sdesc_mnmajor(va, kk), idesc_o, (i >= 2 || kk > 0));
+          umma_bf16_ts(tbase + 384, tbase + b * 128 + kk * 8, sdesc_mnmajor(va, kk), idesc_o,
+                       (i > 0 || kk > 0));
         umma_commit(&sm.pv_done[b]);
         umma_commit(&sm.v_empty[s]);
-        if (i + 2 < nk) issue_s(i + 2);  // same buffer b: in-order after PV_i
+        if (i + 2 < nk) issue_s(i + 2);
       }
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
-    // ------------------------------------------------ softmax warpgroups
-    const int w = wid >> 2;  // warpgroup: tiles i = w, w + 2, ...
-    const int r = (wid & 3) * 32 + lane_id();  // query row within the block == TMEM lane
-    const uint32_t lane_off = (uint32_t)((wid & 3) * 32) << 16;
-    const uint32_t tS = tbase + w * 128 + lane_off;
-    const uint32_t tO = tbase + 256 + w * 128 + lane_off;
-    float m_used = -INFINITY, l = 0.f;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    // ------------------------------------------------ softmax warps 0-7
+    // warp w: TMEM lanes (w & 3) * 32 + (w >> 2) * 16 .. +16; thread: rows
+    // R0 = base + lane / 4 and R0 + 8, columns 8k + 2a, 8k + 2a + 1 (a = lane % 4)
+    const int lbase = (wid & 3) * 32 + (wid >> 2) * 16;
+    const int a = lane_id() & 3;
+    const int R0 = lbase + (lane_id() >> 2);
+    const uint32_t lane_off = (uint32_t)lbase << 16;
+    const uint32_t tO = tbase + 384 + lane_off;
+    float m_used[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
 #ifdef FP_TIMING
     const bool timing_on = (tid == 0);
     long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tlast = clock64();
 #endif
-    for (int i = w; i < nk; i += 2) {
-      const int kb = DENSE ? i : __ldg(list + i);
+    for (int i = 0; i < nk; ++i) {
+      const int b = i % kSBuf;
+      const uint32_t tS = tbase + b * 128 + lane_off;
       FP_TMARK(7);
-      mbar_wait(&sm.s_full[w], (i >> 1) & 1);
+      mbar_wait(&sm.s_full[b], (i / kSBuf) & 1);
       tc_fence_after();
       FP_TMARK(0);
-      float alpha;
-      const float rs = (kb == qb)
-                           ? softmax_tile<true>(tS, tO, r, scale_log2, m_used, alpha, i >= 2 FP_TPASS)
-                           : softmax_tile<false>(tS, tO, r, scale_log2, m_used, alpha, i >= 2 FP_TPASS);
-      l = l * alpha + rs;
-      FP_TMARK(3);
+      float v[64];
+      tmem_ld_16x256b_x16(tS, reinterpret_cast<uint32_t*>(v));
+      tmem_wait_ld();
+      FP_TMARK(1);
+      float alpha[2], rs[2];
+      if (i == nk - 1)  // the diagonal block is the last one of the sorted row
+        softmax_tile<true>(v, R0, a, scale_log2, m_used, alpha, rs);
+      else
+        softmax_tile<false>(v, R0, a, scale_log2, m_used, alpha, rs);
+      FP_TMARK(2);
+      l[0] = l[0] * alpha[0] + rs[0];
+      l[1] = l[1] * alpha[1] + rs[1];
+      if (i > 0 && __any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
+        // O holds sum_{t<i} P_t V_t: wait for PV_{i-1}, rescale this thread's rows
+        mbar_wait(&sm.pv_done[(i - 1) % kSBuf], ((i - 1) / kSBuf) & 1);
+        tc_fence_after();
+        float ov[64];
+        tmem_ld_16x256b_x16(tO, reinterpret_cast<uint32_t*>(ov));
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          ov[4 * k] *= alpha[0];
+          ov[4 * k + 1] *= alpha[0];
+          ov[4 * k + 2] *= alpha[1];
+          ov[4 * k + 3] *= alpha[1];
+        }
+        tmem_st_16x256b_x16(tO, reinterpret_cast<uint32_t*>(ov));
+      }
+      FP_TMARK(4);
+      // P (bf16 pairs): packed column 4k + a holds keys 8k + 2a, 8k + 2a + 1
+      uint32_t pk[32];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        pk[2 * k] = pack_bf16x2(v[4 * k], v[4 * k + 1]);
+        pk[2 * k + 1] = pack_bf16x2(v[4 * k + 2], v[4 * k + 3]);
+      }
+      tmem_st_16x128b_x16(tS, pk);
       tmem_wait_st();
+      FP_TMARK(5);
       tc_fence_before();
-      mbar_arrive(&sm.p_full[w]);
+      mbar_arrive(&sm.p_full[b]);
       FP_TMARK(6);
     }
 #ifdef FP_TIMING
     if (timing_on) {
       for (int k = 0; k < 8; ++k) atomicAdd(&g_attn_timing[k], (unsigned long long)tacc[k]);
-      atomicAdd(&g_attn_timing[8], (unsigned long long)((nk + 1) / 2));
+      atomicAdd(&g_attn_timing[8], (unsigned long long)nk);
     }
 #endif
-    // epilogue: merge the two partial softmaxes, O = (a0 O_0 + a1 O_1) / (a0 l_0 + a1 l_1)
-    const int n_mine = (nk - w + 1) / 2;  // tiles of this warpgroup
-    if (n_mine > 0) {
-      const int i_last = w + 2 * (n_mine - 1);
-      mbar_wait(&sm.pv_done[w], (i_last >> 1) & 1);
-    }
-    sm.ml[w][0][r] = m_used;
-    sm.ml[w][1][r] = l;
-    named_bar_sync(1, 256);
+    // epilogue: O / l -> bf16 -> global
+    const float il0 = 1.0f / quad_sum(l[0]), il1 = 1.0f / quad_sum(l[1]);
+    mbar_wait(&sm.pv_done[(nk - 1) % kSBuf], ((nk - 1) / kSBuf) & 1);
     tc_fence_after();
-    const float m0 = sm.ml[0][0][r], m1 = sm.ml[1][0][r];
-    const float mm = fmaxf(m0, m1);
-    const float a0 = exp2f(m0 - mm);
-    const float a1 = (nk > 1) ? exp2f(m1 - mm) : 0.f;
-    const float inv_l = 1.0f / (a0 * sm.ml[0][1][r] + a1 * sm.ml[1][1][r]);
-    const float f0 = a0 * inv_l, f1 = a1 * inv_l;
-    // this warpgroup writes output columns w*64 .. w*64+63
-    const uint32_t tO0 = tbase + 256 + lane_off + w * 64, tO1 = tbase + 384 + lane_off + w * 64;
-    uint4* dst = reinterpret_cast<uint4*>(o + ((size_t)h * n + (size_t)qb * 128 + r) * 128 + w * 64);
+    float ov[64];
+    tmem_ld_16x256b_x16(tO, reinterpret_cast<uint32_t*>(ov));
+    tmem_wait_ld();
+    uint32_t* d0 = reinterpret_cast<uint32_t*>(o + ((size_t)h * n + (size_t)qb * 128 + R0) * 128) + a;
+    uint32_t* d1 = d0 + 8 * 64;  // row R0 + 8 (64 bf16 pairs per row)
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t o0[32], o1[32];
-      tmem_ld32(tO0 + c * 32, o0);
-      if (nk > 1) tmem_ld32(tO1 + c * 32, o1);
-      tmem_wait_ld();
-      float y[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        y[e] = (nk > 1) ? fmaf(__uint_as_float(o0[e]), f0, __uint_as_float(o1[e]) * f1)
-                        : __uint_as_float(o0[e]) * f0;
-#pragma unroll
-      for (int e = 0; e < 32; e += 8) {
-        uint4 wv;
-        wv.x = pack_bf16x2(y[e], y[e + 1]);
-        wv.y = pack_bf16x2(y[e + 2], y[e + 3]);
-        wv.z = pack_bf16x2(y[e + 4], y[e + 5]);
-        wv.w = pack_bf16x2(y[e + 6], y[e + 7]);
-        dst[(c * 32 + e) / 8] = wv;
-      }
+    for (int k = 0; k < 16; ++k) {
+      d0[4 * k] = pack_bf16x2(ov[4 * k] * il0, ov[4 * k + 1] * il0);
+      d1[4 * k] = pack_bf16x2(ov[4 * k + 2] * il1, ov[4 * k + 3] * il1);
     }
   }
   tc_fence_before();
