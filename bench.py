@@ -347,6 +347,14 @@ def main():
     f_issued = sum(4 * 128 * 128 * 128 * x for x in nnz)
     density = float(np.sum(nnz)) / (len(nnz) * nb * (nb + 1) / 2)
 
+    # ---- the same layer replayed as one CUDA graph (launch overhead excluded)
+    graph_ms = None
+    if len(runs) == 1 and world == 1:
+        r0 = runs[0]
+        graph = r0["fpl"].capture_layer(r0["q"], r0["k"], r0["v"], r0["o"], w.gamma, w.tau,
+                                        w.min_budget)
+        graph_ms, _ = timed(graph.replay, a.steps, 1)
+
     # ---- dense causal baseline (same library)
     dense_ms = None
     if not a.no_dense:
@@ -412,6 +420,7 @@ def main():
                            if world > 1 else "single GPU",
                            l2="inputs 1.5 GiB > L2, plus L2 flush between steps (outside events)"),
             "latency_ms_per_layer": ms_step,
+            "ms_per_step_cuda_graph": graph_ms,
             "stage_ms": {"plan": plan_ms, "select": sel_ms, "attn": attn_ms},
             "dense_ms_per_layer": dense_ms,
             "speedup_vs_dense": (dense_ms / ms_step) if dense_ms else None,

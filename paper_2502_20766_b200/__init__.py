@@ -208,6 +208,22 @@ class FlexPrefill:
         self.select(gamma, min_budget, stream, with_stats=False)
         self.attn(q, k, v, out, stream)
 
+    def capture_layer(self, q, k, v, out, gamma=0.95, tau=0.1, min_budget=0):
+        """Record plan -> select -> attn into one CUDA graph (the C ABI only
+        enqueues on the current stream, so the whole layer is capturable).
+        Returns the torch.cuda.CUDAGraph; replay() reruns the layer on the
+        same buffers."""
+        import torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up outside capture (kernel attributes)
+            self.layer(q, k, v, out, gamma, tau, min_budget)
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.layer(q, k, v, out, gamma, tau, min_budget)
+        return graph
+
     def stats(self):
         raw = bytes(self.stats_buf.cpu().numpy().tobytes())
         arr = (SelectStats * self.H).from_buffer_copy(raw)

@@ -9,10 +9,11 @@
 
 namespace fp {
 
-constexpr int kChunkTiles = 8;  // key tiles (128 keys) per representative-pass CTA
+constexpr int kChunkTilesMax = 8;  // key tiles (128 keys) per representative-pass CTA (max)
 
 struct Shape {
   int H, G, n, nb, nchunks, g;  // g = H / G
+  int ct;                       // key tiles per representative-pass CTA
   long long tri;                // nb (nb + 1) / 2
 };
 
@@ -22,7 +23,11 @@ inline Shape make_shape(int heads, int kv_heads, int seq_len) {
   s.G = kv_heads;
   s.n = seq_len;
   s.nb = seq_len / 128;
-  s.nchunks = (s.nb + kChunkTiles - 1) / kChunkTiles;
+  // largest chunk (<= 8 tiles) that still gives >= 2 CTAs per SM of the
+  // 148-SM B200 for the representative passes (short sequences: smaller chunks)
+  s.ct = kChunkTilesMax;
+  while (s.ct > 1 && (long long)((s.nb + s.ct - 1) / s.ct) * heads < 2 * 148) s.ct >>= 1;
+  s.nchunks = (s.nb + s.ct - 1) / s.ct;
   s.g = heads / kv_heads;
   s.tri = (long long)s.nb * (s.nb + 1) / 2;
   return s;

@@ -14,7 +14,8 @@
 //   block_sums        a_hat[kb] = sum of a_v over kb (A2); As[D] (A12)
 //   pattern_kernel N3 a_bar = softmax(avgpool(Q^) K_bar^T / sqrt d), D_JS, decision
 //   qbar_kernel   N4a avg-pooled Q per block (QA heads only)
-//   pooled_map    N4b A_bar row softmax over kb <= qb, / nb (QA heads only)
+//   pooled_logits N4b block-causal pooled logits, 32x32 tiles (QA heads only)
+//   pooled_softmax N4c A_bar row softmax over kb <= qb, / nb (QA heads only)
 #include <math.h>
 
 #include "fp_common.cuh"
@@ -107,7 +108,7 @@ __device__ float block_max(float v, float* red) {
 template <int PASS>
 __global__ void __launch_bounds__(kRepThreads, 1)
     rep_pass(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-             int H, int G, int n, int nb, int nchunks, float scale_log2, float* __restrict__ m_part,
+             int H, int G, int n, int nb, int nchunks, int ct, float scale_log2, float* __restrict__ m_part,
              float* __restrict__ l_part, const float* __restrict__ m_row,
              const float* __restrict__ il_row, float* __restrict__ k_bar, float* __restrict__ a_v,
              float* __restrict__ as_part) {
@@ -122,8 +123,8 @@ __global__ void __launch_bounds__(kRepThreads, 1)
   const int lane_row = wq * 32 + lane_id();  // TMEM lane of this thread
   const int chunk = blockIdx.x, h = blockIdx.y;
   const int g = h / (H / G);
-  const int t0 = chunk * kChunkTiles;
-  const int ntile = min(kChunkTiles, nb - t0);
+  const int t0 = chunk * ct;
+  const int ntile = min(ct, nb - t0);
   const bool do_kbar = (PASS == 1) && (h % (H / G) == 0);
 
   if (warp_id() == 0) tmem_alloc(&sm.tmem_base, 256);
@@ -401,38 +402,62 @@ __global__ void qbar_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* 
 }
 
 // A_bar[qb, kb <= qb] = softmax_row(scale * Qbar[qb] . Kbar[kb]) / nb  (A5)
-constexpr int kMapThreads = 256;
-__global__ void __launch_bounds__(kMapThreads) pooled_map(
+// Two kernels: pooled_logits computes the block-causal logits tile by tile
+// (32 x 32 block pairs per CTA, Qbar and Kbar tiles staged in shared memory,
+// fp32 FFMA dot products in fixed d order) straight into the packed A_bar
+// rows; pooled_softmax normalises each row in place.
+constexpr int kPT = 32;  // row / column tile of the pooled logits
+__global__ void __launch_bounds__(256) pooled_logits(
     const float* __restrict__ q_bar, const float* __restrict__ k_bar,
     const int32_t* __restrict__ pattern, int H, int G, int nb, float scale,
     float* __restrict__ A_bar) {
-  extern __shared__ float msm[];  // qv[128] | logit[nb] | red[33]
-  const int qb = blockIdx.x, h = blockIdx.y;
-  if (pattern[h] != 1) return;
+  const int rt = blockIdx.x, ct = blockIdx.y, h = blockIdx.z;
+  if (ct > rt || pattern[h] != 1) return;
+  __shared__ float qs[kPT][129];
+  __shared__ float ks[kPT][129];
   const int g = h / (H / G);
-  float* qv = msm;
-  float* logit = msm + 128;
-  float* red = logit + nb;
   const int tid = threadIdx.x;
-  if (tid < 128) qv[tid] = q_bar[((size_t)h * nb + qb) * 128 + tid];
-  __syncthreads();
-  const int w = warp_id(), ln = lane_id();
-  for (int kb = w; kb <= qb; kb += kMapThreads / 32) {
-    const float4 kv = *reinterpret_cast<const float4*>(k_bar + ((size_t)g * nb + kb) * 128 + ln * 4);
-    float d = qv[ln * 4] * kv.x + qv[ln * 4 + 1] * kv.y + qv[ln * 4 + 2] * kv.z + qv[ln * 4 + 3] * kv.w;
-    d = warp_sum(d);
-    if (ln == 0) logit[kb] = d * scale;
+  for (int e = tid; e < kPT * 128; e += 256) {
+    const int rr = e >> 7, d = e & 127;
+    const int qb = rt * kPT + rr, kb = ct * kPT + rr;
+    qs[rr][d] = (qb < nb) ? q_bar[((size_t)h * nb + qb) * 128 + d] : 0.f;
+    ks[rr][d] = (kb < nb) ? k_bar[((size_t)g * nb + kb) * 128 + d] : 0.f;
   }
   __syncthreads();
+  const int rr = tid >> 3, c0 = tid & 7;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+  for (int d = 0; d < 128; ++d) {
+    const float qv = qs[rr][d];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) acc[m] = fmaf(qv, ks[c0 + 8 * m][d], acc[m]);
+  }
+  const int qb = rt * kPT + rr;
+  if (qb >= nb) return;
+  float* row = A_bar + (size_t)h * ((size_t)nb * (nb + 1) / 2) + (size_t)qb * (qb + 1) / 2;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int kb = ct * kPT + c0 + 8 * m;
+    if (kb <= qb) row[kb] = acc[m] * scale;
+  }
+}
+
+constexpr int kMapThreads = 256;
+__global__ void __launch_bounds__(kMapThreads) pooled_softmax(const int32_t* __restrict__ pattern,
+                                                              int nb, float* __restrict__ A_bar) {
+  __shared__ float red[33];
+  const int qb = blockIdx.x, h = blockIdx.y;
+  if (pattern[h] != 1) return;
+  float* row = A_bar + (size_t)h * ((size_t)nb * (nb + 1) / 2) + (size_t)qb * (qb + 1) / 2;
+  const int tid = threadIdx.x;
   float mx = -INFINITY;
-  for (int kb = tid; kb <= qb; kb += kMapThreads) mx = fmaxf(mx, logit[kb]);
+  for (int kb = tid; kb <= qb; kb += kMapThreads) mx = fmaxf(mx, row[kb]);
   mx = block_max<kMapThreads>(mx, red);
   float se = 0.f;
-  for (int kb = tid; kb <= qb; kb += kMapThreads) se += expf(logit[kb] - mx);
+  for (int kb = tid; kb <= qb; kb += kMapThreads) se += expf(row[kb] - mx);
   se = block_sum<kMapThreads>(se, red);
-  float* out = A_bar + (size_t)h * ((size_t)nb * (nb + 1) / 2) + (size_t)qb * (qb + 1) / 2;
   const float inv_nb = 1.0f / (float)nb;
-  for (int kb = tid; kb <= qb; kb += kMapThreads) out[kb] = (expf(logit[kb] - mx) / se) * inv_nb;
+  for (int kb = tid; kb <= qb; kb += kMapThreads) row[kb] = (expf(row[kb] - mx) / se) * inv_nb;
 }
 
 }  // namespace
@@ -460,12 +485,12 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
   float* m_row = wsp<float>(ws, L.m_row);
   float* il_row = wsp<float>(ws, L.il_row);
   dim3 grid(s.nchunks, s.H);
-  rep_pass<1><<<grid, kRepThreads, sm1, st>>>(qmap, kmap, s.H, s.G, s.n, s.nb, s.nchunks, scale_log2,
+  rep_pass<1><<<grid, kRepThreads, sm1, st>>>(qmap, kmap, s.H, s.G, s.n, s.nb, s.nchunks, s.ct, scale_log2,
                                               m_part, l_part, m_row, il_row,
                                               wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_v),
                                               wsp<float>(ws, L.as_part));
   rep_stats<<<s.H, 128, 0, st>>>(s.nchunks, m_part, l_part, m_row, il_row);
-  rep_pass<2><<<grid, kRepThreads, sm2, st>>>(qmap, kmap, s.H, s.G, s.n, s.nb, s.nchunks, scale_log2,
+  rep_pass<2><<<grid, kRepThreads, sm2, st>>>(qmap, kmap, s.H, s.G, s.n, s.nb, s.nchunks, s.ct, scale_log2,
                                               m_part, l_part, m_row, il_row,
                                               wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_v),
                                               wsp<float>(ws, L.as_part));
@@ -482,9 +507,12 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
   qbar_kernel<<<dim3(s.nb, s.H), 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(q),
                                                wsp<int32_t>(ws, L.pattern), s.n, s.nb,
                                                wsp<float>(ws, L.q_bar));
-  pooled_map<<<dim3(s.nb, s.H), kMapThreads, psm, st>>>(
-      wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar), wsp<int32_t>(ws, L.pattern), s.H, s.G,
-      s.nb, scale, wsp<float>(ws, L.A_bar));
+  const int nt = (s.nb + kPT - 1) / kPT;
+  pooled_logits<<<dim3(nt, nt, s.H), 256, 0, st>>>(wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar),
+                                                   wsp<int32_t>(ws, L.pattern), s.H, s.G, s.nb,
+                                                   scale, wsp<float>(ws, L.A_bar));
+  pooled_softmax<<<dim3(s.nb, s.H), kMapThreads, 0, st>>>(wsp<int32_t>(ws, L.pattern), s.nb,
+                                                          wsp<float>(ws, L.A_bar));
   return cudaGetLastError();
 }
 

@@ -62,7 +62,7 @@ __device__ uint64_t block_scan_u64(uint64_t v, uint64_t* wsum, uint64_t* total) 
   return v + add;
 }
 
-constexpr int kCl = 4;  // CTAs (one cluster) per top-mass segment
+constexpr int kCl = 8;  // CTAs (one cluster) per top-mass segment
 
 // distributed shared memory helpers (thread block cluster)
 __device__ __forceinline__ uint32_t cl_rank() {
@@ -144,6 +144,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads, 1)
   bool count_mode = false;
   uint32_t prefix = 0, pmask = 0;
   unsigned long long above_mass_tot = 0, above_cnt_tot = 0;
+  unsigned long long slice_gt = 0, slice_eq = 0;
   const int shifts[3] = {21, 10, 0};
   const int widths[3] = {11, 11, 10};
   for (int pass = 0; pass < 3; ++pass) {
@@ -238,6 +239,18 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads, 1)
       }
     }
     __syncthreads();
+    {
+      // this CTA's slice counts above the chosen digit (and, last pass, equal to
+      // it) from its own histogram: elements > lambda / == lambda in the slice
+      const uint32_t B = sm.found_bin;
+      uint64_t part = 0;
+      if (d0 >= 0 && (uint32_t)d0 > B) part += sm.cnt[d0];
+      if (d1 >= 0 && (uint32_t)d1 > B) part += sm.cnt[d1];
+      uint64_t tot_gt;
+      block_scan_u64(part, sm.wsum, &tot_gt);
+      slice_gt += tot_gt;
+      if (pass == 2) slice_eq = sm.cnt[B];
+    }
     prefix |= sm.found_bin << sh;
     pmask |= dmask << sh;
     above_mass_tot += sm.above_mass;
@@ -252,19 +265,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads, 1)
   const uint64_t K = above_cnt_tot + t_take;
 
   // slice counts (> lambda, == lambda), exchanged across the cluster for the offsets
-  {
-    unsigned long long gt = 0, eq = 0;
-    for (long long i = lo + tid; i < hi; i += kSelThreads) {
-      const uint32_t key = __float_as_uint(x[i]);
-      gt += key > lam;
-      eq += key == lam;
-    }
-    uint64_t tot;
-    block_scan_u64((eq << 32) | gt, sm.wsum, &tot);
-    if (tid == 0) {
-      sm.slice_gt = tot & 0xffffffffu;
-      sm.slice_eq = tot >> 32;
-    }
+  if (tid == 0) {
+    sm.slice_gt = slice_gt;
+    sm.slice_eq = slice_eq;
   }
   cl_sync();
   uint64_t gt_run = 0, eq_run = 0;

@@ -174,6 +174,31 @@ def test_tiny_sequences(fp, n):
     _check_attn_stagewise(w, res, Q, K, V)
 
 
+def test_ragged_chunk_multi_tile(fp):
+    # 65 blocks, 32 heads: 4-tile representative chunks with a 1-tile last chunk
+    w = Workload("ragged-ct4", 32, 8, 8320, 0.9, 0.1, 0, 9)
+    q, k, v = gen.make_layer_bits(w)
+    Q, K, V = parity.oracle_inputs(q, k, v)
+    res = parity.run_gpu(fp, w, q, k, v)
+    _check_plan(w, res, _oracle_plans(w, Q, K, heads=[0, 3, 17, 30]))
+    _check_select_stagewise(w, res, w.gamma, 0)
+
+
+def test_cuda_graph_replay_matches_eager(fp):
+    import torch
+    w = Workload("graph", 8, 2, 4096, 0.9, 0.1, 0, 13)
+    q, k, v = gen.make_layer_bits(w)
+    eager = parity.run_gpu(fp, w, q, k, v)
+    qt, kt, vt = (parity.to_torch_bf16(x) for x in (q, k, v))
+    fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len)
+    out = torch.zeros_like(qt)
+    graph = fpl.capture_layer(qt, kt, vt, out, w.gamma, w.tau, 0)
+    out.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.float().cpu().numpy(), eager["out"])
+
+
 def test_determinism(fp):
     w = Workload("det", 8, 2, 4096, 0.9, 0.1, 0, 5)
     q, k, v = gen.make_layer_bits(w)
