@@ -24,6 +24,7 @@ class Workload:
     seed: int = 0
     head_dim: int = 128
     block: int = 128
+    mixed: bool = False  # C5 tau sweep: mixed QA + vertical heads (synth/gen.py)
 
     def with_(self, **kw):
         return replace(self, **kw)
@@ -40,6 +41,7 @@ class Workload:
             "tau": self.tau,
             "min_budget": self.min_budget,
             "seed": self.seed,
+            "mixed_heads": self.mixed,
         }
 
 
@@ -54,8 +56,8 @@ C3_G09 = C3.with_(name="C3-llama8b-128k-g0.9", gamma=0.9)
 C4 = Workload("C4-glm4-9b-128k", 32, 2, 131072, 0.95, 0.1, 1024, 104)
 C4_GAMMAS = (0.80, 0.85, 0.90, 0.95, 0.97, 0.99)
 # configs[4]: context sweep for Qwen2-7B-like and Yi-9B-like layouts, tau sweep.
-C5_QWEN = Workload("C5-qwen2-7b", 28, 4, 32768, 0.9, 0.1, 0, 105)
-C5_YI = Workload("C5-yi-9b", 32, 4, 32768, 0.9, 0.1, 0, 106)
+C5_QWEN = Workload("C5-qwen2-7b", 28, 4, 32768, 0.9, 0.1, 0, 105, mixed=True)
+C5_YI = Workload("C5-yi-9b", 32, 4, 32768, 0.9, 0.1, 0, 106, mixed=True)
 C5_LENGTHS = (4096, 8192, 16384, 32768, 65536, 131072)
 C5_TAUS = (0.05, 0.1, 0.2, 0.3)
 

@@ -162,7 +162,19 @@ def make_v(seed, H, G, n, g):
     return r.standard_normal((n, D), dtype=np.float32)
 
 
-def make_q(seed, H, G, n, h, gains=GAINS):
+MIX_W = (0.2, 0.45, 0.7, 1.0)  # vertical share of the mixed heads, by KV group (mod 4)
+
+
+def is_mixed(h, heads, kv_heads):
+    g = heads // kv_heads
+    return g > 1 and h % g == 0
+
+
+def make_q(seed, H, G, n, h, gains=GAINS, mixed=False):
+    """Q rows of head h. mixed=True (the C5 tau sweep): the
+    first head of every KV group is Query-Aware-type plus a vertical
+    (heavy-hitter) component of relative weight MIX_W[group % 4], which spreads
+    D_JS across the swept tau range."""
     lam = _lam(n, gains)
     r = _rng(seed, H, G, n, ROLE_Q, h)
     rm = _rng(seed, H, G, n, ROLE_QMETA, h)
@@ -171,12 +183,15 @@ def make_q(seed, H, G, n, h, gains=GAINS):
     pos = np.arange(n, dtype=np.float64)
     # per-head component multipliers so heads of a group differ
     mult = rm.uniform(1.0 - gains["head_jitter"], 1.0 + gains["head_jitter"], 8)
-    if is_qa_type(h, H, G):
+    mix = mixed and is_mixed(h, H, G)
+    if is_qa_type(h, H, G) or mix:
         Q[:, SINK] = _amp(gains["qa_sink"]) * mult[0]
         nb = n // 128
         lam_h = rm.integers(0, N_CLUSTERS, nb)
         qb = np.arange(n) // 128
         Q[np.arange(n), 102 + lam_h[qb]] = _amp(gains["cluster"] + lam) * mult[1]
+        if mix:
+            Q[:, VERT] = MIX_W[(h * G // H) % 4] * _amp(gains["vert"] + lam) * mult[2]
     else:
         Q[:, SINK] = _amp(gains["sink"] + lam) * mult[0]
         Q[:, VERT] = _amp(gains["vert"] + lam) * mult[1]
@@ -200,7 +215,7 @@ def make_layer_bits(w, heads=None, gains=GAINS):
     k = np.zeros((G, n, D), np.uint16)
     v = np.zeros((G, n, D), np.uint16)
     for h in hs:
-        q[h] = bf16_bits(make_q(w.seed, H, G, n, h, gains))
+        q[h] = bf16_bits(make_q(w.seed, H, G, n, h, gains, getattr(w, "mixed", False)))
     for g in gs:
         k[g] = bf16_bits(make_k(w.seed, H, G, n, g, gains))
         v[g] = bf16_bits(make_v(w.seed, H, G, n, g))

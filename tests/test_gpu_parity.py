@@ -245,3 +245,20 @@ def test_layer_host_e2e_matches_device_path(fp):
                      0, fpl.ws, fpl.ws_bytes, fpl.pattern, fpl.jsd, fpl.row_ptr, fpl.col_idx)
     torch.cuda.synchronize()
     assert np.array_equal(oh.float().numpy(), res["out"])
+
+
+def test_tau_sweep_mixed_heads(fp):
+    # C5-style mixed heads spread D across the swept taus; the decision flips per tau
+    from synth.configs import C5_QWEN, C5_TAUS
+    w = C5_QWEN.with_(seq_len=4096)
+    q, k, v = gen.make_layer_bits(w)
+    Q, K, V = parity.oracle_inputs(q, k, v)
+    plans = _oracle_plans(w, Q, K)
+    flips = set()
+    for tau in C5_TAUS:
+        res = parity.run_gpu(fp, w.with_(tau=tau), q, k, v, want_out=False)
+        for h, p in plans.items():
+            assert abs(res["jsd"][h] - p["D"]) <= 1e-4, (tau, h)
+            assert res["pattern"][h] == (1 if p["D"] < tau else 0), (tau, h, p["D"])
+        flips.add(int(res["pattern"].sum()))
+    assert len(flips) >= 3  # the number of QA heads changes across the sweep
