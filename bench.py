@@ -234,7 +234,9 @@ def main():
         if rank == 0:
             print(f"warning: --gpus {a.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local_rank)
-    if world > 1:
+    # torchrun (even with one rank) -> NCCL process group and the output all-gather
+    dist_on = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if dist_on:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     fp.load_library()
     dev = torch.device("cuda", local_rank)
@@ -268,7 +270,7 @@ def main():
     stream = torch.cuda.current_stream()
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
-    full = torch.empty((world * hmax, n, 128), dtype=torch.bfloat16, device=dev) if world > 1 else None
+    full = torch.empty((world * hmax, n, 128), dtype=torch.bfloat16, device=dev) if dist_on else None
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
@@ -285,13 +287,13 @@ def main():
             r["fpl"].attn(r["q"], r["k"], r["v"], r["o"])
             if rec is not None:
                 rec["a1"].append(ev()); rec["a1"][-1].record(stream)
-        if world > 1:
+        if dist_on:
             dist.all_gather_into_tensor(full, out)
 
     def dense_step():
         for r in runs:
             r["fpl"].dense(r["q"], r["k"], r["v"], r["od"])
-        if world > 1:
+        if dist_on:
             dist.all_gather_into_tensor(full, out_dense)
 
     def timed(fn, steps, warmup, rec=None):
@@ -299,7 +301,7 @@ def main():
             flush.zero_()
             fn()
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
         starts, ends = [], []
@@ -309,12 +311,12 @@ def main():
             fn() if rec is None else fn(rec)
             ends.append(ev()); ends[-1].record(stream)
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
         ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
         t_ms = torch.tensor([float(np.mean(ms))], device=dev)
-        if world > 1:
+        if dist_on:
             dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
         return float(t_ms.item()), ms
 
@@ -349,7 +351,7 @@ def main():
 
     # ---- the same layer replayed as one CUDA graph (launch overhead excluded)
     graph_ms = None
-    if len(runs) == 1 and world == 1:
+    if len(runs) == 1 and not dist_on:
         r0 = runs[0]
         graph = r0["fpl"].capture_layer(r0["q"], r0["k"], r0["v"], r0["o"], w.gamma, w.tau,
                                         w.min_budget)
@@ -373,7 +375,7 @@ def main():
                                  h1 - h0, g_hi - g_lo, n, w.gamma, w.tau, w.min_budget,
                                  r0["fpl"].ws, r0["fpl"].ws_bytes, r0["fpl"].pattern,
                                  r0["fpl"].jsd, r0["fpl"].row_ptr, r0["fpl"].col_idx)
-                if world > 1:
+                if dist_on:
                     dist.all_gather_into_tensor(full, out)
             e2e_ms, _ = timed(e2e_step, max(2, min(a.steps, 5)), 1)
             e2e = {"value": n / (e2e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e2e_ms,
@@ -417,7 +419,7 @@ def main():
             "dtype": "bf16",
             "data": "synthetic (seeded planted sink/vertical/slash/diverse structure, synth/gen.py)",
             "config": dict(w.describe(), parallelism=f"heads/{world} + NCCL all-gather of O"
-                           if world > 1 else "single GPU",
+                           if dist_on else "single GPU",
                            l2="inputs 1.5 GiB > L2, plus L2 flush between steps (outside events)"),
             "latency_ms_per_layer": ms_step,
             "ms_per_step_cuda_graph": graph_ms,
@@ -442,7 +444,7 @@ def main():
             "gen_s": t_gen,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
 
