@@ -51,7 +51,14 @@ constexpr int kAttnThreads = 384;      // 8 softmax warps, K producer (8), MMA (
 #endif
 constexpr int kEmuK = FP_EMU / 4;      // of each thread's 16 column groups (4 values), this many
                                        // are exponentiated on the FMA pipe
-constexpr int kSBuf = 3;               // S/P buffers in TMEM
+// FP_QTMEM: copy the Q tile into TMEM once (tcgen05.cp) so S = Q K^T reads only
+// K from shared memory; TMEM then holds 2 S/P buffers + O + Q, and S_(i+2)
+// reuses buffer (i & 1) right after PV_i is issued (in-order tcgen05 stream).
+#ifndef FP_QTMEM
+#define FP_QTMEM 1
+#endif
+constexpr int kSBuf = FP_QTMEM ? 2 : 3;  // S/P buffers in TMEM
+constexpr uint32_t kColO = FP_QTMEM ? 256 : 384, kColQ = 384;
 constexpr int kKV = 3;                 // K and V ring depths
 #ifndef FP_RT
 #define FP_RT 8.0f
@@ -294,17 +301,31 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       auto issue_s = [&](int i) {
         const int s = i % kKV, b = i % kSBuf;
         mbar_wait(&sm.k_full[s], (i / kKV) & 1);
+#if !FP_QTMEM
         // buffer b was last used by tile i-3: its P must have been consumed
         if (i >= kSBuf) mbar_wait(&sm.pv_done[b], ((i - kSBuf) / kSBuf) & 1);
+#endif
         tc_fence_after();
         const uint32_t ka = smem_u32(sm.k[s]);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
+        for (int kk = 0; kk < 8; ++kk) {
+#if FP_QTMEM
+          umma_bf16_ts(tbase + b * 128, tbase + kColQ + kk * 8, sdesc_kmajor(ka, kk), idesc_s, kk > 0);
+#else
           umma_bf16_ss(tbase + b * 128, sdesc_kmajor(qa, kk), sdesc_kmajor(ka, kk), idesc_s, kk > 0);
+#endif
+        }
         umma_commit(&sm.s_full[b]);
         umma_commit(&sm.k_empty[s]);
       };
       mbar_wait(&sm.q_full, 0);
+#if FP_QTMEM
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)  // Q (K-major SW128 in smem) -> TMEM columns kColQ + 8 kk
+        asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tbase + kColQ + kk * 8),
+                     "l"(sdesc_kmajor(qa, kk)));
+#endif
       issue_s(0);
       if (nk > 1) issue_s(1);
       for (int i = 0; i < nk; ++i) {
@@ -315,7 +336,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const uint32_t va = smem_u32(sm.v[s]);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_bf16_ts(tbase + 384, tbase + b * 128 + kk * 8, sdesc_mnmajor(va, kk), idesc_o,
+          umma_bf16_ts(tbase + kColO, tbase + b * 128 + kk * 8, sdesc_mnmajor(va, kk), idesc_o,
                        (i > 0 || kk > 0));
         umma_commit(&sm.pv_done[b]);
         umma_commit(&sm.v_empty[s]);
@@ -332,7 +353,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const int a = lane_id() & 3;
     const int R0 = lbase + (lane_id() >> 2);
     const uint32_t lane_off = (uint32_t)lbase << 16;
-    const uint32_t tO = tbase + 384 + lane_off;
+    const uint32_t tO = tbase + kColO + lane_off;
     float m_used[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
 #ifdef FP_TIMING
     const bool timing_on = (tid == 0);
