@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #endif
         }
         umma_commit(&sm.s_full[b]);
-        umma_commit(&sm.k_empty[s]);
+        if (i + kKV < nk) umma_commit(&sm.k_empty[s]);  // the producer waits only for these
       };
       mbar_wait(&sm.q_full, 0);
 #if FP_QTMEM
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           umma_bf16_ts(tbase + kColO, tbase + b * 128 + kk * 8, sdesc_mnmajor(va, kk), idesc_o,
                        (i > 0 || kk > 0));
         umma_commit(&sm.pv_done[b]);
-        umma_commit(&sm.v_empty[s]);
+        if (i + kKV < nk) umma_commit(&sm.v_empty[s]);
         if (i + 2 < nk) issue_s(i + 2);
       }
     }
@@ -379,9 +379,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       FP_TMARK(2);
       l[0] = l[0] * alpha[0] + rs[0];
       l[1] = l[1] * alpha[1] + rs[1];
+      // every PV completion is consumed (here, normally long complete): O then
+      // holds sum_{t<i} P_t V_t and may be rescaled
+      if (i > 0) mbar_wait(&sm.pv_done[(i - 1) % kSBuf], ((i - 1) / kSBuf) & 1);
       if (i > 0 && __any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
-        // O holds sum_{t<i} P_t V_t: wait for PV_{i-1}, rescale this thread's rows
-        mbar_wait(&sm.pv_done[(i - 1) % kSBuf], ((i - 1) / kSBuf) & 1);
+        // rescale this thread's rows of O
         tc_fence_after();
         float ov[64];
         tmem_ld_16x256b_x16(tO, reinterpret_cast<uint32_t*>(ov));
