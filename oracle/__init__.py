@@ -28,6 +28,10 @@ from .flexprefill import (  # noqa: F401
     add_forced,
     vs_row_scores,
     min_budget_extend,
+    slash_block_sums,
+    vs_block_mask_pooled,
+    qa_rowwise_mask,
+    max_budget_cut,
     sparse_attention,
     dense_causal_attention,
     plan_head,

@@ -235,6 +235,70 @@ def min_budget_extend(M, R, min_budget, b):
     return M
 
 
+# --------------------------------------------- next rows f1 / f2 (variants) ---
+def slash_block_sums(a_s, b):
+    """As[D] = sum of a_s over offsets [D b, (D+1) b) (the A12 row-score term)."""
+    nb = a_s.shape[0] // b
+    return a_s.reshape(nb, b).sum(axis=1)
+
+
+def vs_block_mask_pooled(S_vb, S_db, nb):
+    """f1, reading R2 (block-pooled lines): vertical *blocks* S_vb selected by
+    topmass(a_hat), slash *offset groups* S_db selected by topmass(As). The
+    offsets of group D = [D b, (D+1) b) lie on block diagonals D and D+1 (an
+    element pair (i, i-o) with o in the group has floor(i/b) - floor((i-o)/b)
+    in {D, D+1}), so a selected group marks both; block (qb, kb <= qb) is
+    selected iff kb in S_vb or qb - kb in {D, D+1 : D in S_db}."""
+    Vb = np.zeros(nb, bool)
+    Vb[np.asarray(S_vb, np.int64)] = True
+    Db = np.zeros(nb + 1, bool)
+    S_db = np.asarray(S_db, np.int64)
+    Db[S_db] = True
+    Db[S_db + 1] = True
+    qb = np.arange(nb)[:, None]
+    kb = np.arange(nb)[None, :]
+    return (kb <= qb) & (Vb[kb] | Db[np.clip(qb - kb, 0, nb)])
+
+
+def qa_rowwise_mask(Abar, gamma):
+    """f2 "wo/ flatten": per query block, the smallest set of key
+    blocks whose pooled-estimate mass reaches gamma of that row's mass (the
+    topmass rule of Alg. 4 applied to each row of A_bar instead of the
+    flattened map). Returns (mask, list of per-row topmass results)."""
+    nb = Abar.shape[0]
+    M = np.zeros((nb, nb), bool)
+    per_row = []
+    for qb in range(nb):
+        t = topmass(Abar[qb, : qb + 1], gamma)
+        M[qb, t["sel"]] = True
+        per_row.append(t)
+    return M, per_row
+
+
+def max_budget_cut(M, R, max_budget, b):
+    """f2 maximum budget, read like A12: per query-block row at
+    most m = ceil(max_budget / b) key blocks; rows above the cap keep their
+    forced blocks {0, qb} (never removed) and then the best remaining
+    selected blocks by row score R (descending, ties -> lower kb)."""
+    if max_budget <= 0:
+        return M.copy()
+    M = M.copy()
+    nb = M.shape[0]
+    m = -(-max_budget // b)
+    for qb in range(nb):
+        sel = [kb for kb in range(qb + 1) if M[qb, kb]]
+        forced = {0, qb}
+        cap = max(m, len(forced))
+        if len(sel) <= cap:
+            continue
+        keep = set(forced)
+        rest = sorted((kb for kb in sel if kb not in forced), key=lambda kb: (-R[qb, kb], kb))
+        keep.update(rest[: cap - len(forced)])
+        M[qb, :] = False
+        M[qb, sorted(keep)] = True
+    return M
+
+
 # ------------------------------------------------------------- O10, O11 ------
 def sparse_attention(Qh, Kg, Vg, M, b, qblocks=None):
     """O10: y = A(Q, K, V, S) = softmax((Q K^T + M_S)/sqrt d) V.
@@ -280,35 +344,48 @@ def plan_head(Qh, Kg, b, tau):
     return dict(pattern=decide_pattern(D, tau), D=D, a_v=a_v, a_s=a_s, a_hat=a_hat, a_bar=a_bar)
 
 
-def select_head(plan, Qh, Kg, b, gamma, min_budget):
-    """Alg. 3 or Alg. 4 by pattern, then forced blocks (O8) and min budget (O9)."""
+def select_head(plan, Qh, Kg, b, gamma, min_budget, vs_mode=0, qa_mode=0, max_budget=0):
+    """Alg. 3 or Alg. 4 by pattern, then forced blocks (O8), minimum budget (O9)
+    and maximum budget (f2). vs_mode 1 = block-pooled lines (f1, R2);
+    qa_mode 1 = per-query-block selection (f2, "wo/ flatten")."""
     n = Kg.shape[0]
     nb = n // b
     out = dict()
     if plan["pattern"] == VS:
-        tv = topmass(plan["a_v"], gamma)
-        ts = topmass(plan["a_s"], gamma)
+        if vs_mode == 0:
+            tv = topmass(plan["a_v"], gamma)
+            ts = topmass(plan["a_s"], gamma)
+            M0 = vs_block_mask(tv["sel"], ts["sel"], n, b)
+        else:
+            tv = topmass(plan["a_hat"], gamma)
+            ts = topmass(slash_block_sums(plan["a_s"], b), gamma)
+            M0 = vs_block_mask_pooled(tv["sel"], ts["sel"], nb)
         out.update(tv=tv, ts=ts, S_v=tv["sel"], S_s=ts["sel"])
-        M0 = vs_block_mask(tv["sel"], ts["sel"], n, b)
         R = vs_row_scores(plan["a_hat"], plan["a_s"], b)
     else:
         Abar = qa_pooled_map(Qh, Kg, b)
-        vals, rows, cols = qa_flat(Abar)
-        tq = topmass(vals, gamma)
-        out.update(Abar=Abar, tq=tq, S_qa=tq["sel"])
-        M0 = qa_block_mask(tq["sel"], rows, cols, nb)
+        if qa_mode == 0:
+            vals, rows, cols = qa_flat(Abar)
+            tq = topmass(vals, gamma)
+            out.update(tq=tq, S_qa=tq["sel"])
+            M0 = qa_block_mask(tq["sel"], rows, cols, nb)
+        else:
+            M0, per_row = qa_rowwise_mask(Abar, gamma)
+            out.update(tq_rows=per_row)
+        out.update(Abar=Abar)
         R = np.where(np.tril(np.ones((nb, nb), bool)), Abar, -np.inf)
     M1 = add_forced(M0)
-    M = min_budget_extend(M1, R, min_budget, b)
-    out.update(mask_pre=M0, mask_forced=M1, mask=M, row_score=R)
+    M2 = min_budget_extend(M1, R, min_budget, b)
+    M = max_budget_cut(M2, R, max_budget, b)
+    out.update(mask_pre=M0, mask_forced=M1, mask_min=M2, mask=M, row_score=R)
     return out
 
 
 def flexprefill_head(Qh, Kg, Vg, b=128, gamma=0.9, tau=0.1, min_budget=0, qblocks=None,
-                     with_output=True):
+                     with_output=True, vs_mode=0, qa_mode=0, max_budget=0):
     """Alg. 1 (Sparse Attention) for one Q head."""
     plan = plan_head(Qh, Kg, b, tau)
-    sel = select_head(plan, Qh, Kg, b, gamma, min_budget)
+    sel = select_head(plan, Qh, Kg, b, gamma, min_budget, vs_mode, qa_mode, max_budget)
     res = dict(plan)
     res.update(sel)
     if with_output:

@@ -428,3 +428,87 @@ def test_planted_structure_is_recovered():
             lam = np.argmax(Q[h, -1, 102:118])
             match = [kb for kb in range(nb) if meta["clusters"][kb] == lam]
             assert all(r["mask_pre"][nb - 1, kb] for kb in match)
+
+
+# ------------------------------------------------- f1 / f2 variants ----------
+def brute_vs_blocks_pooled(S_vb, S_db, n, b):
+    """expand vertical blocks to columns and offset groups to offsets, then the
+    element pairs, then OR into blocks."""
+    cols = {j for kb in S_vb for j in range(kb * b, kb * b + b)}
+    offs = {o for D in S_db for o in range(D * b, min(n, D * b + b))}
+    return brute_vs_blocks(cols, offs, n, b)
+
+
+def test_vs_block_mask_pooled_bruteforce():
+    rng = np.random.default_rng(40)
+    n, b = 64, 8
+    for trial in range(25):
+        S_vb = sorted(set(rng.choice(8, int(rng.integers(0, 4)), replace=False).tolist()))
+        S_db = sorted(set(rng.choice(8, int(rng.integers(0, 4)), replace=False).tolist()))
+        M = oracle.vs_block_mask_pooled(S_vb, S_db, n // b)
+        assert np.array_equal(M, brute_vs_blocks_pooled(S_vb, S_db, n, b)), (S_vb, S_db)
+
+
+def test_slash_block_sums_and_pooled_equals_literal_on_aligned_offsets():
+    a_s = np.arange(32, dtype=float)
+    np.testing.assert_allclose(oracle.slash_block_sums(a_s, 8), [28, 92, 156, 220])
+    # selecting every offset of a group at element level (R1) gives the same
+    # blocks as selecting the group (R2)
+    n, b = 64, 8
+    for D in range(8):
+        offs = list(range(D * b, D * b + b))
+        assert np.array_equal(oracle.vs_block_mask([], offs, n, b),
+                              oracle.vs_block_mask_pooled([], [D], n // b))
+
+
+def test_qa_rowwise_mask_properties():
+    Q, K = rnd(41, 128, 8), rnd(42, 128, 8)
+    A = oracle.qa_pooled_map(Q, K, 16)
+    for gamma in (0.5, 0.8, 0.95):
+        M, per_row = oracle.qa_rowwise_mask(A, gamma)
+        for qb in range(8):
+            row = A[qb, : qb + 1]
+            sel = np.nonzero(M[qb])[0]
+            assert np.all(sel <= qb)
+            assert row[sel].sum() >= gamma * row.sum() - 1e-15  # coverage per row
+            k, _ = exhaustive_min_subset(list(row), gamma)  # minimality (Appendix B)
+            assert len(sel) == k
+
+
+def test_max_budget_cut_properties():
+    rng = np.random.default_rng(43)
+    nb, b = 16, 128
+    for trial in range(20):
+        M = oracle.add_forced(np.tril(rng.random((nb, nb)) < 0.6))
+        R = np.where(np.tril(np.ones((nb, nb), bool)), np.round(rng.random((nb, nb)), 1), -np.inf)
+        mb = int(rng.integers(1, 8)) * 128
+        out = oracle.max_budget_cut(M, R, mb, b)
+        m = -(-mb // b)
+        for qb in range(nb):
+            row0, row = M[qb], out[qb]
+            assert np.all(row <= row0)  # only removes
+            assert row[0] and row[qb]  # forced blocks survive
+            cap = max(m, len({0, qb}))
+            assert row.sum() == min(row0.sum(), cap)
+            kept = [kb for kb in np.nonzero(row)[0] if kb not in (0, qb)]
+            dropped = [kb for kb in np.nonzero(row0 & ~row)[0]]
+            for a_ in kept:  # kept blocks beat dropped ones (ties -> lower kb)
+                for z in dropped:
+                    assert (R[qb, a_] > R[qb, z]) or (R[qb, a_] == R[qb, z] and a_ < z)
+    assert np.array_equal(oracle.max_budget_cut(M, R, 0, b), M)
+
+
+def test_variants_reduce_to_defaults():
+    from synth import gen
+    from synth.configs import C1
+    q, k, v = gen.make_layer_bits(C1)
+    Q, K = gen.bits_to_f64(q), gen.bits_to_f64(k)
+    for h in range(C1.heads):
+        p = oracle.plan_head(Q[h], K[0], 128, 0.1)
+        base = oracle.select_head(p, Q[h], K[0], 128, 0.9, 0)
+        big = oracle.select_head(p, Q[h], K[0], 128, 0.9, 0, max_budget=10 ** 9)
+        assert np.array_equal(base["mask"], big["mask"])  # an unreachable cap changes nothing
+        # gamma = 1: every variant selects every causal block
+        for vm, qm in ((1, 0), (0, 1), (1, 1)):
+            full = oracle.select_head(p, Q[h], K[0], 128, 1.0, 0, vs_mode=vm, qa_mode=qm)
+            assert full["mask"].sum() == 16 * 17 // 2
