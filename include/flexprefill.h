@@ -58,15 +58,32 @@ typedef enum {
 } fp_status;
 
 /* Per-head selection statistics (fp_select). k_v / k_s: number of selected
- * vertical / slash lines (K_v, K_s of Alg. 3), 0 for QA heads;
- * k_qa: K of Alg. 4, 0 for VS heads; nnz_blocks: computed (q-block,
- * k-block) pairs after forced blocks and minimum budget; budget_added: blocks
- * added by the minimum budget (A12); mass_*: achieved estimated mass of
+ * vertical / slash lines (K_v, K_s of Alg. 3; block columns /
+ * diagonal groups with vs_mode 1), 0 for QA heads; k_qa: K of Alg. 4 (
+ * summed over rows with qa_mode 1), 0 for VS heads; nnz_blocks: computed
+ * (q-block, k-block) pairs after forced blocks and the budgets; budget_added /
+ * budget_removed: blocks added by the minimum budget (A12) / removed by
+ * the maximum budget (A23); mass_*: achieved estimated mass of
  * the selected lines/blocks (fixed-point sum). */
 typedef struct {
-  int32_t k_v, k_s, k_qa, nnz_blocks, budget_added, pattern;
+  int32_t k_v, k_s, k_qa, nnz_blocks, budget_added, pattern, budget_removed;
   double mass_v, mass_s, mass_qa;
 } fp_select_stats;
+
+/* Selection variants (fp_select_ex).
+ *   vs_mode     0: Vertical-Slash lines selected at element level and rasterised
+ *                  (Alg. 3 as written, reading A10/R1; default)
+ *               1: block-pooled lines (f1, reading A24/R2): key-block columns by
+ *                  topmass(a_hat), slash offset groups [D b, (D+1) b) by
+ *                  topmass(As); a selected group marks block diagonals D, D+1
+ *   qa_mode     0: flatten and normalise the pooled map, one topmass (Alg. 4)
+ *               1: per query block ("wo/ flatten", A25)
+ *   max_budget  tokens per query-block row, 0 = off (A23); rows
+ *               above ceil(max_budget / 128) blocks keep their forced blocks
+ *               and the best remaining blocks by row score */
+typedef struct {
+  int32_t vs_mode, qa_mode, max_budget;
+} fp_select_options;
 
 /* Device pointers into a workspace filled by fp_plan / fp_select (for tests
  * and stage-wise parity; read-only for the caller). Shapes, n = seq_len,
@@ -123,6 +140,14 @@ fp_status fp_plan(const void* q, const void* k, int heads, int kv_heads, int seq
 fp_status fp_select(int heads, int kv_heads, int seq_len, int head_dim, int block_size, float gamma,
                     int min_budget, void* ws, size_t ws_bytes, int32_t* row_ptr, int32_t* col_idx,
                     fp_select_stats* stats, void* stream);
+
+/* fp_select with the selection variants of fp_select_options (NULL = the
+ * defaults, identical to fp_select). FP_ERR_RANGE for a mode outside {0, 1} or
+ * max_budget < 0. */
+fp_status fp_select_ex(int heads, int kv_heads, int seq_len, int head_dim, int block_size,
+                       float gamma, int min_budget, const fp_select_options* opt, void* ws,
+                       size_t ws_bytes, int32_t* row_ptr, int32_t* col_idx, fp_select_stats* stats,
+                       void* stream);
 
 /* Stage (iii): y = softmax((Q K^T + M_S) / sqrt(d)) V over exactly the blocks
  * in the CSR (intersected with j <= i), online softmax, GQA.

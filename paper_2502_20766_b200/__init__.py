@@ -17,7 +17,7 @@ import os
 
 __all__ = [
     "FlexPrefill", "FlexPrefillError", "load_library", "fp_workspace_bytes", "fp_col_idx_capacity",
-    "fp_plan", "fp_select", "fp_sparse_attn", "fp_dense_causal_attn", "fp_layer_host",
+    "fp_plan", "fp_select", "fp_select_ex", "fp_sparse_attn", "SelectOptions", "fp_dense_causal_attn", "fp_layer_host",
     "fp_debug_view", "fp_kernels_per_layer", "LIB_PATH", "SelectStats",
 ]
 
@@ -40,8 +40,16 @@ class FlexPrefillError(RuntimeError):
 class SelectStats(ctypes.Structure):
     _fields_ = [("k_v", ctypes.c_int32), ("k_s", ctypes.c_int32), ("k_qa", ctypes.c_int32),
                 ("nnz_blocks", ctypes.c_int32), ("budget_added", ctypes.c_int32),
-                ("pattern", ctypes.c_int32), ("mass_v", ctypes.c_double),
-                ("mass_s", ctypes.c_double), ("mass_qa", ctypes.c_double)]
+                ("pattern", ctypes.c_int32), ("budget_removed", ctypes.c_int32),
+                ("mass_v", ctypes.c_double), ("mass_s", ctypes.c_double),
+                ("mass_qa", ctypes.c_double)]
+
+
+class SelectOptions(ctypes.Structure):
+    """fp_select_options: vs_mode (0 = element lines, 1 = block-pooled lines, f1),
+    qa_mode (0 = flattened map, 1 = per query block, f2), max_budget (tokens, 0 = off)."""
+    _fields_ = [("vs_mode", ctypes.c_int32), ("qa_mode", ctypes.c_int32),
+                ("max_budget", ctypes.c_int32)]
 
 
 class DebugPtrs(ctypes.Structure):
@@ -68,6 +76,8 @@ def load_library(path=LIB_PATH):
         "fp_col_idx_capacity": (_Z, [_I, _I]),
         "fp_plan": (_I, [_P, _P, _I, _I, _I, _I, _I, _F, _P, _Z, _P, _P, _P]),
         "fp_select": (_I, [_I, _I, _I, _I, _I, _F, _I, _P, _Z, _P, _P, _P, _P]),
+        "fp_select_ex": (_I, [_I, _I, _I, _I, _I, _F, _I, ctypes.POINTER(SelectOptions), _P, _Z,
+                              _P, _P, _P, _P]),
         "fp_sparse_attn": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _Z, _P]),
         "fp_dense_causal_attn": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _Z, _P]),
         "fp_layer_host": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _F, _F, _I,
@@ -137,6 +147,16 @@ def fp_select(heads, kv_heads, seq_len, gamma, min_budget, ws, ws_bytes, row_ptr
                                        _ptr(col_idx), _ptr(stats), _stream(stream)))
 
 
+def fp_select_ex(heads, kv_heads, seq_len, gamma, min_budget, ws, ws_bytes, row_ptr, col_idx,
+                 stats=None, stream=None, vs_mode=0, qa_mode=0, max_budget=0, head_dim=128,
+                 block_size=128):
+    opt = SelectOptions(vs_mode, qa_mode, max_budget)
+    _check("fp_select_ex", _L().fp_select_ex(heads, kv_heads, seq_len, head_dim, block_size, gamma,
+                                             min_budget, ctypes.byref(opt), _ptr(ws), ws_bytes,
+                                             _ptr(row_ptr), _ptr(col_idx), _ptr(stats),
+                                             _stream(stream)))
+
+
 def fp_sparse_attn(q, k, v, o, heads, kv_heads, seq_len, row_ptr, col_idx, ws=None, ws_bytes=0,
                    stream=None, head_dim=128, block_size=128):
     _check("fp_sparse_attn", _L().fp_sparse_attn(_ptr(q), _ptr(k), _ptr(v), _ptr(o), heads, kv_heads,
@@ -192,9 +212,11 @@ class FlexPrefill:
         fp_plan(q, k, self.H, self.G, self.n, tau, self.ws, self.ws_bytes, self.pattern, self.jsd,
                 stream)
 
-    def select(self, gamma=0.95, min_budget=0, stream=None, with_stats=True):
-        fp_select(self.H, self.G, self.n, gamma, min_budget, self.ws, self.ws_bytes, self.row_ptr,
-                  self.col_idx, self.stats_buf if with_stats else None, stream)
+    def select(self, gamma=0.95, min_budget=0, stream=None, with_stats=True, vs_mode=0, qa_mode=0,
+               max_budget=0):
+        fp_select_ex(self.H, self.G, self.n, gamma, min_budget, self.ws, self.ws_bytes,
+                     self.row_ptr, self.col_idx, self.stats_buf if with_stats else None, stream,
+                     vs_mode, qa_mode, max_budget)
 
     def attn(self, q, k, v, out, stream=None):
         fp_sparse_attn(q, k, v, out, self.H, self.G, self.n, self.row_ptr, self.col_idx, self.ws,

@@ -82,7 +82,7 @@ size_t fp_col_idx_capacity(int seq_len, int block_size) {
   return nb * (nb + 1) / 2;
 }
 
-int fp_kernels_per_layer(void) { return 9 + 5 + 1; }
+int fp_kernels_per_layer(void) { return 9 + 6 + 1; }
 
 fp_status fp_plan(const void* q, const void* k, int heads, int kv_heads, int seq_len, int head_dim,
                   int block_size, float tau, void* ws, size_t ws_bytes, int32_t* pattern,
@@ -107,16 +107,28 @@ fp_status fp_plan(const void* q, const void* k, int heads, int kv_heads, int seq
 fp_status fp_select(int heads, int kv_heads, int seq_len, int head_dim, int block_size, float gamma,
                     int min_budget, void* ws, size_t ws_bytes, int32_t* row_ptr, int32_t* col_idx,
                     fp_select_stats* stats, void* stream) {
+  return fp_select_ex(heads, kv_heads, seq_len, head_dim, block_size, gamma, min_budget, nullptr, ws,
+                      ws_bytes, row_ptr, col_idx, stats, stream);
+}
+
+fp_status fp_select_ex(int heads, int kv_heads, int seq_len, int head_dim, int block_size,
+                       float gamma, int min_budget, const fp_select_options* opt_in, void* ws,
+                       size_t ws_bytes, int32_t* row_ptr, int32_t* col_idx, fp_select_stats* stats,
+                       void* stream) {
   if (!ws || !row_ptr || !col_idx) return FP_ERR_NULL;
   fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
   if (st) return st;
   if (!(gamma > 0.f) || isnan(gamma) || min_budget < 0) return FP_ERR_RANGE;
+  fp_select_options opt = {0, 0, 0};
+  if (opt_in) opt = *opt_in;
+  if (opt.vs_mode < 0 || opt.vs_mode > 1 || opt.qa_mode < 0 || opt.qa_mode > 1 || opt.max_budget < 0)
+    return FP_ERR_RANGE;
   if (!aligned16(ws)) return FP_ERR_ALIGN;
   const Shape s = make_shape(heads, kv_heads, seq_len);
   const WsLayout L = ws_layout(s);
   if (ws_bytes < L.total) return FP_ERR_WORKSPACE;
   if ((st = check_device())) return st;
-  return cuda_status(launch_select(s, L, ws, gamma, min_budget, row_ptr, col_idx, stats,
+  return cuda_status(launch_select(s, L, ws, gamma, min_budget, opt, row_ptr, col_idx, stats,
                                    static_cast<cudaStream_t>(stream)));
 }
 

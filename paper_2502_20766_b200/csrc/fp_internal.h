@@ -53,6 +53,8 @@ struct WsLayout {
   size_t rowbits;            // uint32 [H][nb][nbw] final row bitmaps
   size_t row_nnz, row_nnz_pre;  // int32 [H][nb]
   size_t budget_added;       // int32 [H][nb]
+  size_t budget_removed;     // int32 [H][nb]
+  size_t selbits;            // uint32 [H][nb][nbw] per-row QA selection (qa_mode 1)
   size_t sched;              // int32 [64] scheduler scratch
   size_t total;
   int nbw;                   // words per bitmap row
@@ -96,6 +98,8 @@ inline WsLayout ws_layout(const Shape& s) {
   L.row_nnz = take(H * nb * 4);
   L.row_nnz_pre = take(H * nb * 4);
   L.budget_added = take(H * nb * 4);
+  L.budget_removed = take(H * nb * 4);
+  L.selbits = take(H * nb * L.nbw * 4);
   L.sched = take(64 * 4);
   L.total = off;
   return L;
@@ -114,8 +118,8 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
                         const CUtensorMap& qmap, const CUtensorMap& kmap, float tau,
                         int32_t* pattern_out, float* jsd_out, cudaStream_t st);
 cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gamma, int min_budget,
-                          int32_t* row_ptr, int32_t* col_idx, fp_select_stats* stats,
-                          cudaStream_t st);
+                          const fp_select_options& opt, int32_t* row_ptr, int32_t* col_idx,
+                          fp_select_stats* stats, cudaStream_t st);
 cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const CUtensorMap& qmap,
                         const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                         const int32_t* row_ptr, const int32_t* col_idx, bool dense,

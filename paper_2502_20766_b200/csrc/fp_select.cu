@@ -11,7 +11,8 @@
 //                    then an ordered compaction of the selected indices.
 //                    Masses are summed in 2^-60 fixed point (uint64), so every
 //                    sum is exact and order independent (deterministic).
-//   build_lines  N6a vertical-block / slash-diagonal bitmaps (A10, R1)
+//   topmass_rows f2  per query-block row of A_bar (qa_mode 1), row bitmaps
+//   build_lines  N6a vertical-block / slash-diagonal bitmaps (A10 R1; R2 with vs_mode 1)
 //   assemble     N6b per query-block row: rasterised lines or QA blocks,
 //                    forced blocks (A11), minimum budget (A12)
 //   row_scan     N6c per-head CSR row offsets + stats
@@ -104,17 +105,20 @@ struct TopSmem {
 // CTA c of the cluster owns the index slice [c*S, (c+1)*S), S = ceil(L / kCl).
 __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads, 1)
     topmass_kernel(const float* __restrict__ a_v, const float* __restrict__ a_s,
+                   const float* __restrict__ a_hat, const float* __restrict__ As,
                    const float* __restrict__ A_bar, const int32_t* __restrict__ pattern, int n,
-                   long long tri, float gamma, int32_t* __restrict__ sel_v,
-                   int32_t* __restrict__ sel_s, int32_t* __restrict__ sel_qa,
-                   int32_t* __restrict__ sel_count, unsigned long long* __restrict__ sel_mass) {
+                   int nb, long long tri, float gamma, int vs_mode, int qa_mode,
+                   int32_t* __restrict__ sel_v, int32_t* __restrict__ sel_s,
+                   int32_t* __restrict__ sel_qa, int32_t* __restrict__ sel_count,
+                   unsigned long long* __restrict__ sel_mass) {
   extern __shared__ __align__(16) uint8_t top_raw[];
   TopSmem& sm = *reinterpret_cast<TopSmem*>(top_raw);
   const int seg = blockIdx.x / kCl, h = blockIdx.y;
   const uint32_t crank = cl_rank();
   const int tid = threadIdx.x;
   const int pat = pattern[h];
-  if ((pat == 1) != (seg == 2)) {  // whole cluster leaves together
+  // whole cluster leaves together; per-row QA selection (qa_mode 1) is topmass_rows
+  if ((pat == 1) != (seg == 2) || (seg == 2 && qa_mode == 1)) {
     if (tid == 0 && crank == 0) {
       sel_count[h * 4 + seg] = 0;
       sel_mass[h * 4 + seg] = 0;
@@ -124,14 +128,14 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads, 1)
   const float* x;
   int32_t* out;
   long long L;
-  if (seg == 0) {
-    x = a_v + (size_t)h * n;
+  if (seg == 0) {  // vertical lines (a_v) or, vs_mode 1, key-block columns (a_hat)
+    x = vs_mode ? a_hat + (size_t)h * nb : a_v + (size_t)h * n;
     out = sel_v + (size_t)h * n;
-    L = n;
-  } else if (seg == 1) {
-    x = a_s + (size_t)h * n;
+    L = vs_mode ? nb : n;
+  } else if (seg == 1) {  // slash lines (a_s) or, vs_mode 1, offset groups (As)
+    x = vs_mode ? As + (size_t)h * nb : a_s + (size_t)h * n;
     out = sel_s + (size_t)h * n;
-    L = n;
+    L = vs_mode ? nb : n;
   } else {
     x = A_bar + (size_t)h * tri;
     out = sel_qa + (size_t)h * tri;
@@ -314,10 +318,171 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads, 1)
   cl_sync();  // keep this CTA's shared memory alive until the cluster is done
 }
 
+// ---------------------------------------------------------------------------
+// f2 (qa_mode 1, "wo/ flatten"): topmass of each row of A_bar, one
+// CTA of 256 threads per (query block, QA head); same radix select by mass as
+// topmass_kernel (fixed point, ties -> lower kb), output as a row bitmap.
+constexpr int kRowThreads = 256;
+struct RowSmem {
+  uint32_t cnt[2048];
+  unsigned long long mass[2048];
+  uint64_t wsum[32];
+  uint32_t bits[256];  // nb <= 8192 -> 256 words
+  uint32_t found_bin;
+  unsigned long long above_mass, above_cnt;
+};
+
+__device__ uint64_t block_scan_u64_256(uint64_t v, uint64_t* wsum, uint64_t* total) {
+  const int ln = lane_id(), w = warp_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t y = __shfl_up_sync(0xffffffffu, v, o);
+    if (ln >= o) v += y;
+  }
+  if (ln == 31) wsum[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    uint64_t s = (ln < kRowThreads / 32) ? wsum[ln] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (ln >= o) s += y;
+    }
+    if (ln < kRowThreads / 32) wsum[ln] = s;
+  }
+  __syncthreads();
+  const uint64_t add = (w > 0) ? wsum[w - 1] : 0;
+  const uint64_t tot = wsum[kRowThreads / 32 - 1];
+  __syncthreads();
+  *total = tot;
+  return v + add;
+}
+
+__global__ void __launch_bounds__(kRowThreads) topmass_rows(
+    const float* __restrict__ A_bar, const int32_t* __restrict__ pattern, int nb, int nbw,
+    long long tri, float gamma, uint32_t* __restrict__ selbits, int32_t* __restrict__ sel_count,
+    unsigned long long* __restrict__ sel_mass) {
+  __shared__ RowSmem sm;
+  const int qb = blockIdx.x, h = blockIdx.y;
+  if (pattern[h] != 1) return;
+  const float* x = A_bar + (size_t)h * tri + (size_t)qb * (qb + 1) / 2;
+  const int L = qb + 1;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < nbw; i += kRowThreads) sm.bits[i] = 0;
+  unsigned long long T = 0, rem = 0, K = 0, mass_sel = 0;
+  bool count_mode = false, all = false;
+  uint32_t prefix = 0, pmask = 0;
+  unsigned long long above_mass_tot = 0, above_cnt_tot = 0;
+  const int shifts[3] = {21, 10, 0};
+  const int widths[3] = {11, 11, 10};
+  for (int pass = 0; pass < 3 && !all; ++pass) {
+    const int sh = shifts[pass];
+    const uint32_t dmask = (1u << widths[pass]) - 1u;
+    const int nbins = 1 << widths[pass];
+    for (int b = tid; b < 2048; b += kRowThreads) {
+      sm.cnt[b] = 0;
+      sm.mass[b] = 0;
+    }
+    __syncthreads();
+    for (int base = 0; base < L; base += kRowThreads) {
+      const int i = base + tid;
+      const bool valid = i < L;
+      const uint32_t key = valid ? __float_as_uint(x[i]) : 0xffffffffu;
+      const bool match = valid && ((key & pmask) == prefix);
+      const uint32_t digit = match ? ((key >> sh) & dmask) : 0xffffffffu;
+      const uint32_t grp = __match_any_sync(0xffffffffu, digit);
+      if (match) {
+        const uint64_t f = fixp(__uint_as_float(key));
+        const uint32_t s0 = __reduce_add_sync(grp, (uint32_t)(f & 0xFFFFF));
+        const uint32_t s1 = __reduce_add_sync(grp, (uint32_t)((f >> 20) & 0xFFFFF));
+        const uint32_t s2 = __reduce_add_sync(grp, (uint32_t)(f >> 40));
+        if ((__ffs(grp) - 1) == (int)lane_id()) {
+          atomicAdd(&sm.cnt[digit], (uint32_t)__popc(grp));
+          atomicAdd(&sm.mass[digit], ((unsigned long long)s2 << 40) +
+                                         ((unsigned long long)s1 << 20) + (unsigned long long)s0);
+        }
+      }
+    }
+    __syncthreads();
+    // thread t owns the 8 digits nbins-1-8t .. nbins-8-8t (descending)
+    uint64_t km[8], kc[8], pm = 0, pc = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int d = nbins - 1 - 8 * tid - j;
+      km[j] = (d >= 0) ? sm.mass[d] : 0;
+      kc[j] = (d >= 0) ? sm.cnt[d] : 0;
+      pm += km[j];
+      pc += kc[j];
+    }
+    uint64_t tot_m, tot_c;
+    uint64_t excl_m = block_scan_u64_256(pm, sm.wsum, &tot_m) - pm;
+    uint64_t excl_c = block_scan_u64_256(pc, sm.wsum, &tot_c) - pc;
+    if (pass == 0) {
+      T = tot_m;
+      if (gamma >= 1.0f) {  // A7: everything
+        all = true;
+        K = L;
+        mass_sel = T;
+        break;
+      }
+      const unsigned long long G = (unsigned long long)ceil((double)gamma * (double)T);
+      count_mode = (G == 0);
+      rem = count_mode ? 1ull : G;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint64_t q = count_mode ? kc[j] : km[j];
+      const uint64_t e = count_mode ? excl_c : excl_m;
+      if (nbins - 1 - 8 * tid - j >= 0 && e < rem && rem <= e + q) {
+        sm.found_bin = nbins - 1 - 8 * tid - j;
+        sm.above_mass = excl_m;
+        sm.above_cnt = excl_c;
+      }
+      excl_m += km[j];
+      excl_c += kc[j];
+    }
+    __syncthreads();
+    prefix |= sm.found_bin << sh;
+    pmask |= dmask << sh;
+    above_mass_tot += sm.above_mass;
+    above_cnt_tot += sm.above_cnt;
+    rem -= count_mode ? sm.above_cnt : sm.above_mass;
+    __syncthreads();
+  }
+  uint32_t lam = prefix;
+  uint64_t t_take = 0;
+  if (!all) {
+    const uint64_t f_lam = fixp(__uint_as_float(lam));
+    t_take = count_mode ? rem : (rem + f_lam - 1) / f_lam;
+    K = above_cnt_tot + t_take;
+    mass_sel = above_mass_tot + t_take * f_lam;
+  }
+  // selection bits in index order (ties: the first t_take occurrences of lambda)
+  uint64_t eq_run = 0;
+  for (int base = 0; base < L; base += kRowThreads) {
+    const int i = base + tid;
+    const bool valid = i < L;
+    const uint32_t key = valid ? __float_as_uint(x[i]) : 0u;
+    const bool eq = valid && !all && key == lam;
+    uint64_t tot;
+    const uint64_t excl = block_scan_u64_256(eq ? 1 : 0, sm.wsum, &tot) - (eq ? 1 : 0);
+    const bool take = valid && (all || key > lam || (eq && eq_run + excl < t_take));
+    if (take) atomicOr(&sm.bits[i >> 5], 1u << (i & 31));
+    eq_run += tot;
+  }
+  __syncthreads();
+  uint32_t* dst = selbits + ((size_t)h * nb + qb) * nbw;
+  for (int i = tid; i < nbw; i += kRowThreads) dst[i] = sm.bits[i];
+  if (tid == 0) {
+    atomicAdd(&sel_count[h * 4 + 2], (int32_t)K);
+    atomicAdd(&sel_mass[h * 4 + 2], mass_sel);
+  }
+}
+
 // vertical-block and slash-diagonal bitmaps of VS heads (A10, reading R1)
 __global__ void build_lines(const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_v,
                             const int32_t* __restrict__ sel_s, const int32_t* __restrict__ sel_count,
-                            int n, int nb, int nbw, uint32_t* __restrict__ vbits,
+                            int n, int nb, int nbw, int vs_mode, uint32_t* __restrict__ vbits,
                             uint32_t* __restrict__ dbits) {
   extern __shared__ uint32_t bsm[];  // V[nbw] | D[nbw]
   const int h = blockIdx.x;
@@ -330,14 +495,16 @@ __global__ void build_lines(const int32_t* __restrict__ pattern, const int32_t* 
     const int32_t* sv = sel_v + (size_t)h * n;
     const int32_t* ss = sel_s + (size_t)h * n;
     for (int i = threadIdx.x; i < kv; i += blockDim.x) {
-      const int kb = sv[i] >> 7;
+      const int kb = vs_mode ? sv[i] : (sv[i] >> 7);
       atomicOr(&V[kb >> 5], 1u << (kb & 31));
     }
     for (int i = threadIdx.x; i < ks; i += blockDim.x) {
       const int o = ss[i];
-      const int d = o >> 7;
+      const int d = vs_mode ? o : (o >> 7);
       atomicOr(&Dg[d >> 5], 1u << (d & 31));
-      if ((o & 127) && d + 1 < nb) atomicOr(&Dg[(d + 1) >> 5], 1u << ((d + 1) & 31));
+      // R1: offset o crosses diagonals o/b and o/b + 1 (unless aligned);
+      // R2 (vs_mode 1): the offset group [d b, (d+1) b) covers d and d + 1
+      if ((vs_mode || (o & 127)) && d + 1 < nb) atomicOr(&Dg[(d + 1) >> 5], 1u << ((d + 1) & 31));
     }
   }
   __syncthreads();
@@ -356,14 +523,17 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows(
     const uint32_t* __restrict__ dbits, const int32_t* __restrict__ sel_qa,
     const int32_t* __restrict__ sel_count, const float* __restrict__ a_hat,
     const float* __restrict__ As, const float* __restrict__ A_bar, int nb, int nbw,
-    long long tri, int min_blocks, uint32_t* __restrict__ rowbits, int32_t* __restrict__ row_nnz,
-    int32_t* __restrict__ row_nnz_pre, int32_t* __restrict__ budget_added) {
-  extern __shared__ uint32_t asmem[];  // [kAsmWarps][nbw]
+    long long tri, int min_blocks, int qa_mode, const uint32_t* __restrict__ selbits,
+    int max_blocks, uint32_t* __restrict__ rowbits, int32_t* __restrict__ row_nnz,
+    int32_t* __restrict__ row_nnz_pre, int32_t* __restrict__ budget_added,
+    int32_t* __restrict__ budget_removed) {
+  extern __shared__ uint32_t asmem[];  // [kAsmWarps][2][nbw]
   const int h = blockIdx.y;
   const int w = warp_id(), ln = lane_id();
   const int qb = blockIdx.x * kAsmWarps + w;
   if (qb >= nb) return;
-  uint32_t* row = asmem + w * nbw;
+  uint32_t* row = asmem + w * 2 * nbw;
+  uint32_t* keep = row + nbw;
   const int pat = pattern[h];
   const uint32_t* V = vbits + (size_t)h * nbw;
   const uint32_t* Dg = dbits + (size_t)h * nbw;
@@ -377,6 +547,10 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows(
       const uint32_t word = __ballot_sync(0xffffffffu, on);
       if (ln == 0) row[wd] = word;
     }
+  } else if (qa_mode == 1) {
+    // per-row selection already as a bitmap (topmass_rows)
+    const uint32_t* src = selbits + ((size_t)h * nb + qb) * nbw;
+    for (int i = ln; i < nw_row; i += 32) row[i] = src[i];
   } else {
     // S_qa is sorted; this row's flat indices are [qb(qb+1)/2, qb(qb+1)/2 + qb]
     const int kq = sel_count[h * 4 + 2];
@@ -432,34 +606,79 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows(
     __syncwarp();
   }
   const int added = need > 0 ? need : 0;
+  // maximum budget (A23): rows above the cap keep the forced blocks and the
+  // best remaining selected blocks by row score (ties -> lower kb)
+  int removed = 0;
+  const int nforced = (qb == 0) ? 1 : 2;
+  const int cap = max(max_blocks, nforced);
+  if (max_blocks > 0 && pre + added > cap) {
+    for (int i = ln; i < nbw; i += 32) keep[i] = 0;
+    __syncwarp();
+    if (ln == 0) {
+      keep[0] |= 1u;
+      keep[qb >> 5] |= 1u << (qb & 31);
+    }
+    __syncwarp();
+    for (int it = 0; it < cap - nforced; ++it) {
+      float best = -INFINITY;
+      int bkb = 0x7fffffff;
+      for (int kb = ln; kb <= qb; kb += 32) {
+        if (!bit_at(row, kb) || bit_at(keep, kb)) continue;
+        const float sc = (pat == 0) ? __fadd_rn(a_hat[(size_t)h * nb + kb], As[(size_t)h * nb + qb - kb])
+                                    : Ab[kb];
+        if (sc > best || (sc == best && kb < bkb)) {
+          best = sc;
+          bkb = kb;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ok = __shfl_xor_sync(0xffffffffu, bkb, o);
+        if (ob > best || (ob == best && ok < bkb)) {
+          best = ob;
+          bkb = ok;
+        }
+      }
+      if (ln == 0) keep[bkb >> 5] |= 1u << (bkb & 31);
+      __syncwarp();
+    }
+    for (int i = ln; i < nbw; i += 32) row[i] = keep[i];
+    __syncwarp();
+    removed = pre + added - cap;
+  }
   uint32_t* dst = rowbits + ((size_t)h * nb + qb) * nbw;
   for (int i = ln; i < nbw; i += 32) dst[i] = row[i];
   if (ln == 0) {
-    row_nnz[(size_t)h * nb + qb] = pre + added;
+    row_nnz[(size_t)h * nb + qb] = pre + added - removed;
     row_nnz_pre[(size_t)h * nb + qb] = pre;
     budget_added[(size_t)h * nb + qb] = added;
+    budget_removed[(size_t)h * nb + qb] = removed;
   }
 }
 
 // exclusive scan of row nnz per head -> row_ptr; stats
 __global__ void __launch_bounds__(kSelThreads, 1)
     row_scan(const int32_t* __restrict__ row_nnz, const int32_t* __restrict__ budget_added,
+             const int32_t* __restrict__ budget_removed,
              const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_count,
              const unsigned long long* __restrict__ sel_mass, int nb, int32_t* __restrict__ row_ptr,
              fp_select_stats* __restrict__ stats) {
   __shared__ uint64_t wsum[32];
   const int h = blockIdx.x;
-  uint64_t run = 0, badd = 0;
+  uint64_t run = 0, badd = 0, brem = 0;
   for (int base = 0; base < nb; base += kSelThreads) {
     const int i = base + threadIdx.x;
     const uint64_t v = (i < nb) ? (uint64_t)row_nnz[(size_t)h * nb + i] : 0;
     const uint64_t ba = (i < nb) ? (uint64_t)budget_added[(size_t)h * nb + i] : 0;
-    uint64_t tot;
+    const uint64_t br = (i < nb) ? (uint64_t)budget_removed[(size_t)h * nb + i] : 0;
+    uint64_t tot, tot2;
     const uint64_t packed = (ba << 32) | v;
     const uint64_t incl = block_scan_u64(packed, wsum, &tot);
+    block_scan_u64(br, wsum, &tot2);
     if (i < nb) row_ptr[(size_t)h * (nb + 1) + i] = (int32_t)(run + ((incl - packed) & 0xffffffffu));
     run += tot & 0xffffffffu;
     badd += tot >> 32;
+    brem += tot2;
   }
   if (threadIdx.x == 0) {
     row_ptr[(size_t)h * (nb + 1) + nb] = (int32_t)run;
@@ -475,6 +694,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
       st.mass_qa = (double)sel_mass[h * 4 + 2] * inv;
       st.nnz_blocks = (int32_t)run;
       st.budget_added = (int32_t)badd;
+      st.budget_removed = (int32_t)brem;
       stats[h] = st;
     }
   }
@@ -501,8 +721,8 @@ __global__ void __launch_bounds__(kAsmWarps * 32) write_cols(
 }  // namespace
 
 cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gamma, int min_budget,
-                          int32_t* row_ptr, int32_t* col_idx, fp_select_stats* stats,
-                          cudaStream_t st) {
+                          const fp_select_options& opt, int32_t* row_ptr, int32_t* col_idx,
+                          fp_select_stats* stats, cudaStream_t st) {
   const int32_t* pat = wsp<int32_t>(ws, L.pattern);
   static bool attr_done = false;
   if (!attr_done) {
@@ -511,22 +731,32 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
     attr_done = true;
   }
   topmass_kernel<<<dim3(3 * kCl, s.H), kSelThreads, sizeof(TopSmem), st>>>(
-      wsp<float>(ws, L.a_v), wsp<float>(ws, L.a_s), wsp<float>(ws, L.A_bar), pat, s.n, s.tri, gamma,
+      wsp<float>(ws, L.a_v), wsp<float>(ws, L.a_s), wsp<float>(ws, L.a_hat), wsp<float>(ws, L.As),
+      wsp<float>(ws, L.A_bar), pat, s.n, s.nb, s.tri, gamma, opt.vs_mode, opt.qa_mode,
       wsp<int32_t>(ws, L.sel_v), wsp<int32_t>(ws, L.sel_s), wsp<int32_t>(ws, L.sel_qa),
       wsp<int32_t>(ws, L.sel_count), wsp<unsigned long long>(ws, L.sel_mass));
+  if (opt.qa_mode == 1)
+    topmass_rows<<<dim3(s.nb, s.H), kRowThreads, 0, st>>>(
+        wsp<float>(ws, L.A_bar), pat, s.nb, L.nbw, s.tri, gamma, wsp<uint32_t>(ws, L.selbits),
+        wsp<int32_t>(ws, L.sel_count), wsp<unsigned long long>(ws, L.sel_mass));
   build_lines<<<s.H, 1024, 2 * L.nbw * 4, st>>>(pat, wsp<int32_t>(ws, L.sel_v),
                                                 wsp<int32_t>(ws, L.sel_s),
                                                 wsp<int32_t>(ws, L.sel_count), s.n, s.nb, L.nbw,
-                                                wsp<uint32_t>(ws, L.vbits), wsp<uint32_t>(ws, L.dbits));
+                                                opt.vs_mode, wsp<uint32_t>(ws, L.vbits),
+                                                wsp<uint32_t>(ws, L.dbits));
   const int min_blocks = (min_budget + 127) / 128;
+  const int max_blocks = (opt.max_budget + 127) / 128;
   const dim3 rg((s.nb + kAsmWarps - 1) / kAsmWarps, s.H);
-  assemble_rows<<<rg, kAsmWarps * 32, kAsmWarps * L.nbw * 4, st>>>(
+  assemble_rows<<<rg, kAsmWarps * 32, kAsmWarps * 2 * L.nbw * 4, st>>>(
       pat, wsp<uint32_t>(ws, L.vbits), wsp<uint32_t>(ws, L.dbits), wsp<int32_t>(ws, L.sel_qa),
       wsp<int32_t>(ws, L.sel_count), wsp<float>(ws, L.a_hat), wsp<float>(ws, L.As),
-      wsp<float>(ws, L.A_bar), s.nb, L.nbw, s.tri, min_blocks, wsp<uint32_t>(ws, L.rowbits),
-      wsp<int32_t>(ws, L.row_nnz), wsp<int32_t>(ws, L.row_nnz_pre), wsp<int32_t>(ws, L.budget_added));
+      wsp<float>(ws, L.A_bar), s.nb, L.nbw, s.tri, min_blocks, opt.qa_mode,
+      wsp<uint32_t>(ws, L.selbits), max_blocks, wsp<uint32_t>(ws, L.rowbits),
+      wsp<int32_t>(ws, L.row_nnz), wsp<int32_t>(ws, L.row_nnz_pre), wsp<int32_t>(ws, L.budget_added),
+      wsp<int32_t>(ws, L.budget_removed));
   row_scan<<<s.H, kSelThreads, 0, st>>>(wsp<int32_t>(ws, L.row_nnz), wsp<int32_t>(ws, L.budget_added),
-                                        pat, wsp<int32_t>(ws, L.sel_count),
+                                        wsp<int32_t>(ws, L.budget_removed), pat,
+                                        wsp<int32_t>(ws, L.sel_count),
                                         wsp<unsigned long long>(ws, L.sel_mass), s.nb, row_ptr, stats);
   write_cols<<<rg, kAsmWarps * 32, 0, st>>>(wsp<uint32_t>(ws, L.rowbits), row_ptr, s.nb, L.nbw,
                                             s.tri, col_idx);

@@ -21,7 +21,7 @@ def to_torch_bf16(bits, device="cuda"):
 
 
 def run_gpu(fp, w, q_bits, k_bits, v_bits, gamma=None, tau=None, min_budget=None, dense=False,
-            want_out=True):
+            want_out=True, vs_mode=0, qa_mode=0, max_budget=0):
     """Run plan -> select -> attn through the binding; return host copies."""
     import torch
     gamma = w.gamma if gamma is None else gamma
@@ -30,7 +30,7 @@ def run_gpu(fp, w, q_bits, k_bits, v_bits, gamma=None, tau=None, min_budget=None
     q, k, v = (to_torch_bf16(x) for x in (q_bits, k_bits, v_bits))
     fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len)
     fpl.plan(q, k, tau)
-    fpl.select(gamma, min_budget)
+    fpl.select(gamma, min_budget, vs_mode=vs_mode, qa_mode=qa_mode, max_budget=max_budget)
     out = torch.empty_like(q)
     if want_out:
         fpl.attn(q, k, v, out)
@@ -108,17 +108,23 @@ def rel_close(a, b, rtol, floor):
     return float(rel.max(initial=0.0)), float(small.max(initial=0.0))
 
 
-def stagewise_mask(pattern, dbg, h, n, gamma, min_budget, b=128):
-    """Oracle O6-O9 applied to the GPU's own line/QA sets and fp32 scores.
+def stagewise_mask(pattern, dbg, h, n, gamma, min_budget, b=128, vs_mode=0, qa_mode=0,
+                   max_budget=0):
+    """Oracle O6-O9 (and the f1/f2 variants) applied to the GPU's own line/QA
+    sets and fp32 scores.
 
-    The minimum-budget order is decided in fp32 like the kernel (A12 score
-    a_hat[kb] + As[qb-kb] rounded to fp32; QA: A_bar in fp32)."""
+    The budget orders are decided in fp32 like the kernel (A12 score
+    a_hat[kb] + As[qb-kb] rounded to fp32; QA: A_bar in fp32). For the
+    per-row QA mode the oracle's per-row topmass runs on the GPU's fp32 A_bar."""
     nb = n // b
     cnt = dbg["sel_count"][h]
     if pattern == oracle.VS:
         S_v = dbg["sel_v"][h, : cnt[0]]
         S_s = dbg["sel_s"][h, : cnt[1]]
-        M0 = oracle.vs_block_mask(S_v, S_s, n, b)
+        if vs_mode == 0:
+            M0 = oracle.vs_block_mask(S_v, S_s, n, b)
+        else:
+            M0 = oracle.vs_block_mask_pooled(S_v, S_s, nb)
         ah = dbg["a_hat"][h].astype(np.float32)
         As = dbg["As"][h].astype(np.float32)
         qb = np.arange(nb)[:, None]
@@ -127,10 +133,14 @@ def stagewise_mask(pattern, dbg, h, n, gamma, min_budget, b=128):
         R = np.where(kb <= qb, R, -np.inf)
     else:
         vals, rows, cols = oracle.qa_flat(np.zeros((nb, nb)))
-        S_qa = dbg["sel_qa"][h, : cnt[2]]
-        M0 = oracle.qa_block_mask(S_qa, rows, cols, nb)
         A = np.full((nb, nb), -np.inf)
         A[rows, cols] = dbg["A_bar"][h, : len(rows)].astype(np.float64)
+        if qa_mode == 0:
+            S_qa = dbg["sel_qa"][h, : cnt[2]]
+            M0 = oracle.qa_block_mask(S_qa, rows, cols, nb)
+        else:
+            M0, _ = oracle.qa_rowwise_mask(np.where(np.isfinite(A), A, 0.0), gamma)
         R = A
     M1 = oracle.add_forced(M0)
-    return M0, oracle.min_budget_extend(M1, R, min_budget, b)
+    M2 = oracle.min_budget_extend(M1, R, min_budget, b)
+    return M0, oracle.max_budget_cut(M2, R, max_budget, b)

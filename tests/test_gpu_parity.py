@@ -262,3 +262,42 @@ def test_tau_sweep_mixed_heads(fp):
             assert res["pattern"][h] == (1 if p["D"] < tau else 0), (tau, h, p["D"])
         flips.add(int(res["pattern"].sum()))
     assert len(flips) >= 3  # the number of QA heads changes across the sweep
+
+
+@pytest.mark.parametrize("vs_mode,qa_mode,min_budget,max_budget",
+                         [(1, 0, 0, 0), (0, 1, 0, 0), (1, 1, 1024, 0), (0, 0, 0, 1024),
+                          (1, 1, 512, 768)])
+def test_selection_variants_stagewise(fp, vs_mode, qa_mode, min_budget, max_budget):
+    """f1 (block-pooled VS lines), f2 (per-row QA selection, maximum budget):
+    stage-wise parity of the sets and the CSR, attention on the result."""
+    w = Workload("variants", 8, 2, 4096, 0.9, 0.1, min_budget, 17)
+    q, k, v = gen.make_layer_bits(w)
+    Q, K, V = parity.oracle_inputs(q, k, v)
+    res = parity.run_gpu(fp, w, q, k, v, vs_mode=vs_mode, qa_mode=qa_mode, max_budget=max_budget)
+    dbg = res["dbg"]
+    nb = w.seq_len // 128
+    assert set(res["pattern"].tolist()) == {0, 1}
+    for h in range(w.heads):
+        pat = res["pattern"][h]
+        cnt = dbg["sel_count"][h]
+        if pat == oracle.VS:
+            if vs_mode == 1:
+                segs = ((dbg["a_hat"][h], dbg["sel_v"][h, : cnt[0]]),
+                        (dbg["As"][h], dbg["sel_s"][h, : cnt[1]]))
+            else:
+                segs = ((dbg["a_v"][h], dbg["sel_v"][h, : cnt[0]]),
+                        (dbg["a_s"][h], dbg["sel_s"][h, : cnt[1]]))
+            for x, sel in segs:
+                mi, eo, bd, _ = parity.classify(x.astype(np.float64), w.gamma, sel, parity.STAGE_DELTA, 0.0)
+                assert mi == 0 and eo == 0 and bd == 0, (h, vs_mode)
+        M0, M = parity.stagewise_mask(pat, dbg, h, w.seq_len, w.gamma, min_budget, vs_mode=vs_mode,
+                                      qa_mode=qa_mode, max_budget=max_budget)
+        rp, ci = res["row_ptr"][h], res["col_idx"][h]
+        assert parity.csr_rows_sorted(rp, ci, nb)
+        assert np.array_equal(parity.csr_mask(rp, ci, nb), M), (h, vs_mode, qa_mode)
+        if max_budget:
+            m = -(-max_budget // 128)
+            assert np.all(np.diff(rp) <= np.maximum(m, 2))
+    if max_budget:
+        assert sum(s["budget_removed"] for s in res["stats"]) > 0
+    _check_attn_stagewise(w, res, Q, K, V, qblocks=[0, 1, 15, 31])
