@@ -80,3 +80,19 @@ def test_binding_raises_without_fallback(lib):
         pytest.skip("GPU present")
     with pytest.raises(Exception):
         fp.FlexPrefill(4, 1, 2048)
+
+
+def test_select_ex_option_validation(lib):
+    ws_bytes = fp.fp_workspace_bytes(4, 1, 2048)
+    P = 0x10000
+    s = ctypes.c_void_p(0)
+    for bad in [(2, 0, 0), (0, -1, 0), (0, 0, -128)]:
+        opt = fp.SelectOptions(*bad)
+        assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 0, ctypes.byref(opt), P, ws_bytes, P, P,
+                                None, s) == 3, bad
+    import torch
+    if not torch.cuda.is_available():  # valid options -> device check
+        opt = fp.SelectOptions(1, 1, 4096)
+        assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 0, ctypes.byref(opt), P, ws_bytes, P, P,
+                                None, s) == 6
+        assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 0, None, P, ws_bytes, P, P, None, s) == 6

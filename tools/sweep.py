@@ -27,7 +27,8 @@ def useful_flops(nnz, nb):
     return sum(4 * 128 * (128 * 128 * (int(x) - nb) + nb * 128 * 129 // 2) for x in nnz)
 
 
-def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flush=None):
+def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flush=None, opts=None):
+    opts = opts or {}
     st = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
@@ -49,12 +50,12 @@ def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flus
 
     def layer():
         fpl.plan(q, k, w.tau)
-        fpl.select(w.gamma, w.min_budget, with_stats=False)
+        fpl.select(w.gamma, w.min_budget, with_stats=False, **opts)
         fpl.attn(q, k, v, out)
 
     ms = timed(layer, steps, warmup)
     fpl.plan(q, k, w.tau)
-    fpl.select(w.gamma, w.min_budget)
+    fpl.select(w.gamma, w.min_budget, **opts)
     torch.cuda.synchronize()
     a, b = ev(), ev()
     a.record(st)
@@ -69,7 +70,7 @@ def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flus
     dms = timed(lambda: fpl.dense(q, k, v, out), max(2, steps // 2), 1) if dense else None
     return {
         "workload": w.name, "heads": w.heads, "kv_heads": w.kv_heads, "seq_len": w.seq_len,
-        "gamma": w.gamma, "tau": w.tau, "min_budget": w.min_budget,
+        "gamma": w.gamma, "tau": w.tau, "min_budget": w.min_budget, "select_options": opts,
         "layer_ms": ms, "tokens_per_s": w.seq_len / (ms / 1e3), "attn_ms": attn_ms,
         "dense_ms": dms, "speedup_vs_dense": (dms / ms) if dms else None,
         "density": float(np.sum(nnz)) / (len(nnz) * nb * (nb + 1) / 2),
@@ -85,6 +86,10 @@ def points(which):
     if which == "c3":
         for g in (0.9, 0.95):
             yield C.C3.with_(gamma=g), None
+    elif which == "variants":  # next rows f1 / f2 at C3
+        for g in (0.9, 0.95):
+            for o in ({"vs_mode": 1}, {"qa_mode": 1}, {"max_budget": 16384}, {"max_budget": 32768}):
+                yield C.C3.with_(gamma=g), o
     elif which == "c4":
         for mb in (1024, 0):
             for g in C.C4_GAMMAS:
@@ -105,7 +110,7 @@ def main():
     cache = {}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     f = open(out_path, "a") if out_path else None
-    for w, _ in points(which):
+    for w, opts in points(which):
         key = (w.heads, w.kv_heads, w.seq_len, w.seed)
         if key not in cache:
             cache.clear()
@@ -119,7 +124,7 @@ def main():
             print(f"# generated {key} in {time.time() - t:.1f}s", file=sys.stderr, flush=True)
         q, k, v, fpl, out = cache[key]
         steps = 5 if w.seq_len >= 65536 else 10
-        r = measure(fp, torch, w, q, k, v, fpl, out, steps=steps, warmup=2, flush=flush)
+        r = measure(fp, torch, w, q, k, v, fpl, out, steps=steps, warmup=2, flush=flush, opts=opts)
         line = json.dumps(r)
         print(line, flush=True)
         if f:
