@@ -19,6 +19,8 @@
 //   write_cols   N6d CSR column indices (ascending kb)
 #include <math.h>
 
+#include <algorithm>
+
 #include "fp_common.cuh"
 #include "fp_internal.h"
 
@@ -63,7 +65,7 @@ __device__ uint64_t block_scan_u64(uint64_t v, uint64_t* wsum, uint64_t* total) 
   return v + add;
 }
 
-constexpr int kCl = 8;  // CTAs (one cluster) per top-mass segment
+constexpr int kClMax = 8;  // max CTAs (one cluster) per top-mass segment; chosen per launch
 
 // distributed shared memory helpers (thread block cluster)
 __device__ __forceinline__ uint32_t cl_rank() {
@@ -93,7 +95,7 @@ __device__ __forceinline__ unsigned long long cl_ld64(uint32_t a) {
 struct TopSmem {
   uint32_t cnt[2048];             // this CTA's histogram of its slice
   unsigned long long mass[2048];
-  uint32_t gcnt[2048];            // cluster-wide histogram (sum over the kCl CTAs)
+  uint32_t gcnt[2048];            // cluster-wide histogram (sum over the cluster's CTAs)
   unsigned long long gmass[2048];
   uint64_t wsum[32];
   uint32_t found_bin;
@@ -101,9 +103,10 @@ struct TopSmem {
   unsigned long long slice_gt, slice_eq;  // compaction counts of this CTA's slice
 };
 
-// topmass(x, gamma) of one segment by a cluster of kCl CTAs; see file header.
-// CTA c of the cluster owns the index slice [c*S, (c+1)*S), S = ceil(L / kCl).
-__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads, 1)
+// topmass(x, gamma) of one segment by a cluster of ncl CTAs (1..8, set at
+// launch from the segment length); see file header. CTA c of the cluster owns
+// the index slice [c*S, (c+1)*S), S = ceil(L / ncl).
+__global__ void __launch_bounds__(kSelThreads, 1)
     topmass_kernel(const float* __restrict__ a_v, const float* __restrict__ a_s,
                    const float* __restrict__ a_hat, const float* __restrict__ As,
                    const float* __restrict__ A_bar, const int32_t* __restrict__ pattern, int n,
@@ -113,6 +116,9 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kSelThreads, 1)
                    unsigned long long* __restrict__ sel_mass) {
   extern __shared__ __align__(16) uint8_t top_raw[];
   TopSmem& sm = *reinterpret_cast<TopSmem*>(top_raw);
+  uint32_t ncl;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+  const int kCl = (int)ncl;
   const int seg = blockIdx.x / kCl, h = blockIdx.y;
   const uint32_t crank = cl_rank();
   const int tid = threadIdx.x;
@@ -730,11 +736,32 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
                          (int)sizeof(TopSmem));
     attr_done = true;
   }
-  topmass_kernel<<<dim3(3 * kCl, s.H), kSelThreads, sizeof(TopSmem), st>>>(
-      wsp<float>(ws, L.a_v), wsp<float>(ws, L.a_s), wsp<float>(ws, L.a_hat), wsp<float>(ws, L.As),
-      wsp<float>(ws, L.A_bar), pat, s.n, s.nb, s.tri, gamma, opt.vs_mode, opt.qa_mode,
-      wsp<int32_t>(ws, L.sel_v), wsp<int32_t>(ws, L.sel_s), wsp<int32_t>(ws, L.sel_qa),
-      wsp<int32_t>(ws, L.sel_count), wsp<unsigned long long>(ws, L.sel_mass));
+  {
+    // cluster size from the longest segment: ~64K scores per CTA, 1..8 CTAs
+    const long long lmax = std::max<long long>(opt.vs_mode ? s.nb : s.n, opt.qa_mode ? 0 : s.tri);
+    int ncl = 1;
+    while (ncl < kClMax && (long long)ncl * 65536 < lmax) ncl <<= 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(3 * ncl, s.H);
+    cfg.blockDim = dim3(kSelThreads);
+    cfg.dynamicSmemBytes = sizeof(TopSmem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ncl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(
+        &cfg, topmass_kernel, (const float*)wsp<float>(ws, L.a_v), (const float*)wsp<float>(ws, L.a_s),
+        (const float*)wsp<float>(ws, L.a_hat), (const float*)wsp<float>(ws, L.As),
+        (const float*)wsp<float>(ws, L.A_bar), pat, s.n, s.nb, s.tri, gamma, (int)opt.vs_mode,
+        (int)opt.qa_mode, wsp<int32_t>(ws, L.sel_v), wsp<int32_t>(ws, L.sel_s),
+        wsp<int32_t>(ws, L.sel_qa), wsp<int32_t>(ws, L.sel_count),
+        wsp<unsigned long long>(ws, L.sel_mass));
+    if (e != cudaSuccess) return e;
+  }
   if (opt.qa_mode == 1)
     topmass_rows<<<dim3(s.nb, s.H), kRowThreads, 0, st>>>(
         wsp<float>(ws, L.A_bar), pat, s.nb, L.nbw, s.tri, gamma, wsp<uint32_t>(ws, L.selbits),
