@@ -168,8 +168,11 @@ fp_status fp_dense_causal_attn(const void* q, const void* k, const void* v, void
 
 /* The whole layer (Alg. 1) from HOST buffers: copies q/k/v host->device into
  * the caller's device buffers (d_q, d_k, d_v), runs plan/select/attn, and
- * copies the output back to o_host; everything enqueued on `stream` (the copy
- * is asynchronous only if the host buffers are pinned). */
+ * copies the output back to o_host. Pipelined per KV group: the host->device
+ * copy of group c+1 and the device->host copy of group c-1 overlap the compute
+ * of group c on internal streams, joined back into `stream` before return
+ * (ws must hold fp_workspace_bytes of the whole layer; pattern, jsd, row_ptr,
+ * col_idx are the full-layer arrays). Overlap needs pinned host buffers. */
 fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_host, void* o_host,
                         void* d_q, void* d_k, void* d_v, void* d_o, int heads, int kv_heads,
                         int seq_len, int head_dim, int block_size, float gamma, float tau,

@@ -174,26 +174,95 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
                         int seq_len, int head_dim, int block_size, float gamma, float tau,
                         int min_budget, void* ws, size_t ws_bytes, int32_t* pattern, float* jsd,
                         int32_t* row_ptr, int32_t* col_idx, void* stream) {
-  if (!q_host || !k_host || !v_host || !o_host || !d_q || !d_k || !d_v || !d_o) return FP_ERR_NULL;
+  if (!q_host || !k_host || !v_host || !o_host || !d_q || !d_k || !d_v || !d_o || !ws || !pattern ||
+      !jsd || !row_ptr || !col_idx)
+    return FP_ERR_NULL;
   fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
   if (st) return st;
+  if (!(gamma > 0.f) || isnan(gamma) || !(tau >= 0.f && tau <= 1.f) || min_budget < 0)
+    return FP_ERR_RANGE;
+  if (ws_bytes < fp_workspace_bytes(heads, kv_heads, seq_len, head_dim, block_size))
+    return FP_ERR_WORKSPACE;
+  if ((st = check_device())) return st;
+  // Pipelined per KV group (g = heads / kv_heads Q heads + their K/V): host->
+  // device copies of group c+1 and the device->host copy of group c-1 overlap
+  // the compute of group c (three streams joined back to `stream`). Groups use
+  // two workspace slots (the full-layer workspace holds at least two).
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
-  const size_t qbytes = (size_t)heads * seq_len * 128 * 2, kbytes = (size_t)kv_heads * seq_len * 128 * 2;
-  cudaError_t e;
-  if ((e = cudaMemcpyAsync(d_q, q_host, qbytes, cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(d_k, k_host, kbytes, cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
-      (e = cudaMemcpyAsync(d_v, v_host, kbytes, cudaMemcpyHostToDevice, cs)) != cudaSuccess)
-    return cuda_status(e);
-  if ((st = fp_plan(d_q, d_k, heads, kv_heads, seq_len, head_dim, block_size, tau, ws, ws_bytes,
-                    pattern, jsd, stream)))
-    return st;
-  if ((st = fp_select(heads, kv_heads, seq_len, head_dim, block_size, gamma, min_budget, ws, ws_bytes,
-                      row_ptr, col_idx, nullptr, stream)))
-    return st;
-  if ((st = fp_sparse_attn(d_q, d_k, d_v, d_o, heads, kv_heads, seq_len, head_dim, block_size,
-                           row_ptr, col_idx, ws, ws_bytes, stream)))
-    return st;
-  return cuda_status(cudaMemcpyAsync(o_host, d_o, qbytes, cudaMemcpyDeviceToHost, cs));
+  const int g = heads / kv_heads;
+  const size_t n = (size_t)seq_len, nb = n / 128, cap = nb * (nb + 1) / 2;
+  const size_t qb_bytes = (size_t)g * n * 128 * 2, kv_bytes = n * 128 * 2;
+  const size_t slot = align256(fp_workspace_bytes(g, 1, seq_len, head_dim, block_size));
+  const int nslots = (kv_heads > 1 && ws_bytes >= 2 * slot) ? 2 : 1;
+  cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
+  cudaEvent_t e_start = nullptr, e_done = nullptr;
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t r) {
+    if (e == cudaSuccess && r != cudaSuccess) e = r;
+    return e == cudaSuccess;
+  };
+  chk(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
+  chk(cudaStreamCreateWithFlags(&scomp, cudaStreamNonBlocking));
+  chk(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
+  chk(cudaEventCreateWithFlags(&e_start, cudaEventDisableTiming));
+  chk(cudaEventCreateWithFlags(&e_done, cudaEventDisableTiming));
+  if (e == cudaSuccess) {
+    chk(cudaEventRecord(e_start, cs));
+    chk(cudaStreamWaitEvent(sin, e_start, 0));
+    chk(cudaStreamWaitEvent(scomp, e_start, 0));
+    chk(cudaStreamWaitEvent(sout, e_start, 0));
+  }
+  for (int c = 0; c < kv_heads && e == cudaSuccess && st == FP_OK; ++c) {
+    const char* qh = static_cast<const char*>(q_host) + c * qb_bytes;
+    const char* kh = static_cast<const char*>(k_host) + c * kv_bytes;
+    const char* vh = static_cast<const char*>(v_host) + c * kv_bytes;
+    char* qd = static_cast<char*>(d_q) + c * qb_bytes;
+    char* kd = static_cast<char*>(d_k) + c * kv_bytes;
+    char* vd = static_cast<char*>(d_v) + c * kv_bytes;
+    char* od = static_cast<char*>(d_o) + c * qb_bytes;
+    cudaEvent_t e_in = nullptr, e_cmp = nullptr;
+    chk(cudaEventCreateWithFlags(&e_in, cudaEventDisableTiming));
+    chk(cudaEventCreateWithFlags(&e_cmp, cudaEventDisableTiming));
+    chk(cudaMemcpyAsync(kd, kh, kv_bytes, cudaMemcpyHostToDevice, sin));
+    chk(cudaMemcpyAsync(qd, qh, qb_bytes, cudaMemcpyHostToDevice, sin));
+    chk(cudaMemcpyAsync(vd, vh, kv_bytes, cudaMemcpyHostToDevice, sin));
+    chk(cudaEventRecord(e_in, sin));
+    chk(cudaStreamWaitEvent(scomp, e_in, 0));
+    if (e == cudaSuccess) {
+      void* wsc = static_cast<char*>(ws) + (c % nslots) * slot;
+      int32_t* rp = row_ptr + (size_t)c * g * (nb + 1);
+      int32_t* ci = col_idx + (size_t)c * g * cap;
+      if (!(st = fp_plan(qd, kd, g, 1, seq_len, head_dim, block_size, tau, wsc, slot, pattern + c * g,
+                         jsd + c * g, scomp)) &&
+          !(st = fp_select(g, 1, seq_len, head_dim, block_size, gamma, min_budget, wsc, slot, rp, ci,
+                           nullptr, scomp)))
+        st = fp_sparse_attn(qd, kd, vd, od, g, 1, seq_len, head_dim, block_size, rp, ci, wsc, slot,
+                            scomp);
+    }
+    chk(cudaEventRecord(e_cmp, scomp));
+    chk(cudaStreamWaitEvent(sout, e_cmp, 0));
+    chk(cudaMemcpyAsync(static_cast<char*>(o_host) + c * qb_bytes, od, qb_bytes,
+                        cudaMemcpyDeviceToHost, sout));
+    if (e_in) cudaEventDestroy(e_in);
+    if (e_cmp) cudaEventDestroy(e_cmp);
+  }
+  // join everything back into the caller's stream
+  if (e == cudaSuccess) {
+    cudaEvent_t e_c = nullptr;
+    chk(cudaEventCreateWithFlags(&e_c, cudaEventDisableTiming));
+    chk(cudaEventRecord(e_c, scomp));
+    chk(cudaStreamWaitEvent(sout, e_c, 0));
+    chk(cudaEventRecord(e_done, sout));
+    chk(cudaStreamWaitEvent(cs, e_done, 0));
+    if (e_c) cudaEventDestroy(e_c);
+  }
+  if (sin) cudaStreamDestroy(sin);
+  if (scomp) cudaStreamDestroy(scomp);
+  if (sout) cudaStreamDestroy(sout);
+  if (e_start) cudaEventDestroy(e_start);
+  if (e_done) cudaEventDestroy(e_done);
+  if (st) return st;
+  return cuda_status(e);
 }
 
 fp_status fp_debug_view(const void* ws, int heads, int kv_heads, int seq_len, int head_dim,
