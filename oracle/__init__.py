@@ -5,7 +5,7 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 (paper_2502_20766_b200/) never imports it and shares no code with it.
 
 Citations: P:n = /root/reference/PAPER.md line n (read at build time, not at
-run time); A1..A22 = the readings listed in DESIGN.md §3.
+run time); A1..A26 = the readings listed in DESIGN.md §3.
 
 Every function here is pinned by a -m "not gpu" test in tests/test_oracle_*.py
 against something other than itself (closed forms, scipy/torch library

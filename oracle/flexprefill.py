@@ -4,7 +4,7 @@ TEST INFRASTRUCTURE -- see oracle/__init__.py. Slow and obvious on purpose:
 each function is one step of Alg. 1-4 of the paper written in the
 paper's order and notation, using numpy float64 on the exact values of the
 bf16 inputs. No blocking, fusion or reordering beyond what the definitions
-state. Readings of silent / ambiguous passages are tagged A1..A22.
+state. Readings of silent / ambiguous passages are tagged A1..A26.
 """
 import math
 import numpy as np
@@ -56,16 +56,24 @@ def line_scores(Ahat, b):
         # offsets o = 0..p_r pick A^[r, p_r - o]
         a_s[: p_r + 1] += Ahat[r, p_r::-1]
     a_s /= total
-    # sumpool over key blocks of each row's softmax, averaged over the b rows (A2)
-    a_hat = Ahat.reshape(nrep, n // b, b).sum(axis=2).mean(axis=0)
+    # sumpool over key blocks of each row's softmax, averaged over the b rows (A2);
+    # a ragged last block (n % b != 0) is pooled over its actual keys (A26)
+    nb = num_blocks(n, b)
+    a_hat = np.array([Ahat[:, kb * b:(kb + 1) * b].sum(axis=1).mean() for kb in range(nb)])
     return a_v, a_s, a_hat
 
 
 # -------------------------------------------------------------------- O4 -----
+def num_blocks(n, b):
+    """N_b = ceil(n / b): a ragged last block holds the n mod b trailing positions (A26)."""
+    return -(-n // b)
+
+
 def block_mean(X, b):
-    """avgpool with kernel = stride = block_size along the sequence (A3)."""
+    """avgpool with kernel = stride = block_size along the sequence (P:195, A3);
+    a ragged last block averages over its actual rows (A26)."""
     n, d = X.shape
-    return X.reshape(n // b, b, d).mean(axis=1)
+    return np.array([X[kb * b:(kb + 1) * b].mean(axis=0) for kb in range(num_blocks(n, b))])
 
 
 def estimated_block_dist(Qh, Kg, b):
@@ -139,8 +147,9 @@ def vs_block_mask(S_v, S_s, n, b):
     slash o      -> block diagonals floor(o/b), and floor(o/b)+1 if o mod b != 0
                     (a slash at offset o crosses those two block diagonals);
     block (qb, kb <= qb) is selected iff kb in Vb or qb - kb in Db.
+    For ragged n the rule is applied on the b-aligned block grid (A26).
     """
-    nb = n // b
+    nb = num_blocks(n, b)
     Vb = np.zeros(nb, bool)
     Vb[np.asarray(S_v, np.int64) // b] = True
     Db = np.zeros(nb + 1, bool)
@@ -164,7 +173,7 @@ def qa_pooled_map(Qh, Kg, b):
     Returns the (N_b, N_b) map with zeros above the diagonal.
     """
     n, d = Kg.shape
-    nb = n // b
+    nb = num_blocks(n, b)
     L = block_mean(Qh, b) @ block_mean(Kg, b).T / math.sqrt(d)
     A = np.zeros((nb, nb))
     for qb in range(nb):
@@ -205,7 +214,7 @@ def vs_row_scores(a_hat, a_s, b):
     """Row score used by the VS minimum-budget extension (A12):
     score(qb, kb) = a^[kb] + As[qb - kb], As[D] = sum of a_s over [D b, (D+1) b)."""
     nb = a_hat.shape[0]
-    As = a_s.reshape(nb, b).sum(axis=1)
+    As = slash_block_sums(a_s, b)
     qb = np.arange(nb)[:, None]
     kb = np.arange(nb)[None, :]
     R = a_hat[kb] + As[np.clip(qb - kb, 0, nb - 1)]
@@ -237,9 +246,10 @@ def min_budget_extend(M, R, min_budget, b):
 
 # --------------------------------------------- next rows f1 / f2 (variants) ---
 def slash_block_sums(a_s, b):
-    """As[D] = sum of a_s over offsets [D b, (D+1) b) (the A12 row-score term)."""
-    nb = a_s.shape[0] // b
-    return a_s.reshape(nb, b).sum(axis=1)
+    """As[D] = sum of a_s over offsets [D b, (D+1) b) (the A12 row-score term);
+    the last group holds the offsets < n only (A26)."""
+    nb = num_blocks(a_s.shape[0], b)
+    return np.array([a_s[D * b:(D + 1) * b].sum() for D in range(nb)])
 
 
 def vs_block_mask_pooled(S_vb, S_db, nb):
@@ -307,12 +317,13 @@ def sparse_attention(Qh, Kg, Vg, M, b, qblocks=None):
     Returns the (n, d) output (rows of q-blocks not in `qblocks` left NaN).
     """
     n, d = Qh.shape
-    nb = n // b
+    nb = num_blocks(n, b)
     out = np.full((n, d), np.nan)
     for qb in range(nb) if qblocks is None else qblocks:
         kbs = np.nonzero(M[qb, : qb + 1])[0]
         keys = (kbs[:, None] * b + np.arange(b)[None, :]).reshape(-1)
-        qi = np.arange(qb * b, (qb + 1) * b)
+        keys = keys[keys < n]  # ragged last block (A26)
+        qi = np.arange(qb * b, min((qb + 1) * b, n))
         S = Qh[qi] @ Kg[keys].T / math.sqrt(d)
         S[keys[None, :] > qi[:, None]] = -np.inf
         S = S - S.max(axis=1, keepdims=True)
@@ -349,7 +360,7 @@ def select_head(plan, Qh, Kg, b, gamma, min_budget, vs_mode=0, qa_mode=0, max_bu
     and maximum budget (f2). vs_mode 1 = block-pooled lines (f1, R2);
     qa_mode 1 = per-query-block selection (f2, "wo/ flatten")."""
     n = Kg.shape[0]
-    nb = n // b
+    nb = num_blocks(n, b)
     out = dict()
     if plan["pattern"] == VS:
         if vs_mode == 0:

@@ -108,7 +108,7 @@ def _lam(n, gains=GAINS):
 def kv_meta(seed, H, G, n, g, gains=GAINS):
     """Per-KV-head planted structure: vertical columns, far shift, warm blocks, clusters."""
     r = _rng(seed, H, G, n, ROLE_KVMETA, g)
-    nb = n // 128
+    nb = -(-n // 128)  # ragged n: the last block is partial
     # heavy hitters grow with context: n_vert * (n/2048)^vert_growth
     scale = (max(n, 2048) / 2048.0) ** gains["vert_growth"]
     nv = int(r.integers(gains["n_vert"][0], gains["n_vert"][1] + 1) * scale)
@@ -150,7 +150,7 @@ def make_k(seed, H, G, n, g, gains=GAINS):
     pos = np.arange(n, dtype=np.float64)
     K[:, LOCAL] = _dirichlet(pos, K_AMP, gains["period1"])
     K[:, FAR] = _dirichlet(pos, K_AMP, gains["period2"])
-    K[:, WARM] = K_AMP * np.repeat(meta["warm"], 128)
+    K[:, WARM] = K_AMP * np.repeat(meta["warm"], 128)[:n]
     K[0:4, WARM] = 0.0
     kb = np.arange(n) // 128
     K[np.arange(n), 102 + meta["clusters"][kb]] = K_AMP
@@ -186,7 +186,7 @@ def make_q(seed, H, G, n, h, gains=GAINS, mixed=False):
     mix = mixed and is_mixed(h, H, G)
     if is_qa_type(h, H, G) or mix:
         Q[:, SINK] = _amp(gains["qa_sink"]) * mult[0]
-        nb = n // 128
+        nb = -(-n // 128)  # ragged n: the last block is partial
         lam_h = rm.integers(0, N_CLUSTERS, nb)
         qb = np.arange(n) // 128
         Q[np.arange(n), 102 + lam_h[qb]] = _amp(gains["cluster"] + lam) * mult[1]

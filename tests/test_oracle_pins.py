@@ -512,3 +512,129 @@ def test_variants_reduce_to_defaults():
         for vm, qm in ((1, 0), (0, 1), (1, 1)):
             full = oracle.select_head(p, Q[h], K[0], 128, 1.0, 0, vs_mode=vm, qa_mode=qm)
             assert full["mask"].sum() == 16 * 17 // 2
+
+
+# ------------------------------------------------- ragged n (next row f3) ----
+def test_block_pooling_ragged_spec_examples():
+    """sum pooling of [1,3,5,7] by 2 and avg pooling of a
+    5-entry row by 2 (the ragged last cell averages its single entry)."""
+    g = GOLD["block_pool_sum_1357"]
+    a = np.array(g["row"], float)[None, :]
+    _, _, ah = oracle.line_scores(a / a.sum(), g["block"])  # sumpool of the (1-row) map
+    np.testing.assert_allclose(ah * a.sum(), g["sum"], rtol=1e-15)
+    g = GOLD["block_pool_avg_ragged5"]
+    X = np.array(g["row"], float)[:, None]
+    np.testing.assert_allclose(F.block_mean(X, g["block"])[:, 0], g["avg"], rtol=1e-15)
+    assert F.num_blocks(5, 2) == 3 and F.num_blocks(4, 2) == 2
+
+
+@pytest.mark.parametrize("n,b", [(27, 8), (33, 8), (17, 16)])
+def test_ragged_plan_bruteforce(n, b):
+    """O2/O3/O4 on ragged n: the brute-force double loops (written without
+    blocks), a^ = blocksum(a_v) over the actual keys, sum a^ = 1, and the
+    naive pooled estimate with the last key block averaged over its rows."""
+    d = 4
+    Q, K = rnd(60 + n, n, d), rnd(61 + n, n, d)
+    A = oracle.rep_attention(Q, K, b)
+    np.testing.assert_allclose(A, brute_rep_attention(Q, K, b), rtol=1e-12, atol=1e-15)
+    av, as_, ah = oracle.line_scores(A, b)
+    bv, bs = brute_line_scores(A, b)
+    np.testing.assert_allclose(av, bv, rtol=1e-12, atol=1e-16)
+    np.testing.assert_allclose(as_, bs, rtol=1e-12, atol=1e-16)
+    nb = -(-n // b)
+    assert len(ah) == nb
+    blocksum = [sum(av[j] for j in range(n) if j // b == kb) for kb in range(nb)]
+    np.testing.assert_allclose(ah, blocksum, rtol=1e-12, atol=1e-17)
+    assert abs(ah.sum() - 1) < 1e-12
+    qbar = [sum(Q[n - b + r, t] for r in range(b)) / b for t in range(d)]
+    kbar = []
+    for kb in range(nb):
+        rows = [j for j in range(n) if j // b == kb]
+        kbar.append([sum(K[j, t] for j in rows) / len(rows) for t in range(d)])
+    lg = [sum(qbar[t] * kbar[kb][t] for t in range(d)) / math.sqrt(d) for kb in range(nb)]
+    e = [math.exp(x) for x in lg]
+    np.testing.assert_allclose(oracle.estimated_block_dist(Q, K, b), np.array(e) / sum(e), rtol=1e-12)
+    # the pooled map's last row is still a_bar / N_b (the pooled last query block
+    # is the mean of its actual rows, which differs from avgpool(Q^) when ragged)
+    Ab = oracle.qa_pooled_map(Q, K, b)
+    np.testing.assert_allclose(Ab.sum(1), 1.0 / nb)
+    Qb = [[sum(Q[i, t] for i in range(n) if i // b == qb) / len([i for i in range(n) if i // b == qb])
+           for t in range(d)] for qb in range(nb)]
+    for qb in range(nb):
+        lg = [sum(Qb[qb][t] * kbar[kb][t] for t in range(d)) / math.sqrt(d) for kb in range(qb + 1)]
+        e = [math.exp(x) for x in lg]
+        np.testing.assert_allclose(Ab[qb, : qb + 1], np.array(e) / sum(e) / nb, rtol=1e-12)
+
+
+def brute_vs_blocks_padded(S_v, S_s, n, b):
+    """A26: lines expanded to element pairs on the b-aligned (padded) grid
+    [0, N_b b)^2, then OR-ed into blocks."""
+    nb = -(-n // b)
+    M = np.zeros((nb, nb), bool)
+    for i in range(nb * b):
+        for j in range(i + 1):
+            if j in S_v or (i - j) in S_s:
+                M[i // b, j // b] = True
+    return M
+
+
+def test_vs_block_mask_ragged_bruteforce():
+    rng = np.random.default_rng(62)
+    for trial in range(25):
+        n, b = int(rng.integers(41, 64)), 8
+        S_v = set(rng.choice(n, int(rng.integers(0, 6)), replace=False).tolist())
+        S_s = set(rng.choice(n, int(rng.integers(0, 6)), replace=False).tolist())
+        M = oracle.vs_block_mask(sorted(S_v), sorted(S_s), n, b)
+        assert np.array_equal(M, brute_vs_blocks_padded(S_v, S_s, n, b)), (n, S_v, S_s)
+        if n % b == 0:
+            assert np.array_equal(M, brute_vs_blocks(S_v, S_s, n, b))
+
+
+def test_ragged_slash_block_sums_and_row_scores():
+    a_s = np.arange(7, dtype=float)  # offsets 0..6, b = 3 -> groups [0,3), [3,6), [6,7)
+    np.testing.assert_allclose(F.slash_block_sums(a_s, 3), [3.0, 12.0, 6.0])
+    R = oracle.vs_row_scores(np.array([0.5, 0.3, 0.2]), a_s, 3)
+    assert R[2, 0] == 0.5 + 6.0 and R[2, 2] == 0.2 + 3.0 and R[1, 2] == -np.inf
+
+
+@pytest.mark.parametrize("n,b", [(27, 8), (65, 16)])
+def test_ragged_sparse_attention_explicit_mask_and_bound(n, b):
+    """O10 on ragged n against the explicit element mask, the full
+    block set against torch SDPA (library), and the Appendix A bound."""
+    d = 8
+    Q, K, V = rnd(63 + n, n, d, scale=1.5), rnd(64 + n, n, d), rnd(65 + n, n, d)
+    nb = -(-n // b)
+    rng = np.random.default_rng(66)
+    M = oracle.add_forced(np.tril(rng.random((nb, nb)) < 0.4))
+    E = np.kron(M, np.ones((b, b), bool))[:n, :n] & np.tril(np.ones((n, n), bool))
+    out = oracle.sparse_attention(Q, K, V, M, b)
+    np.testing.assert_allclose(out, masked_softmax_attention(Q, K, V, E), rtol=1e-10, atol=1e-12)
+    full = np.tril(np.ones((nb, nb), bool))
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.tensor(Q)[None], torch.tensor(K)[None], torch.tensor(V)[None], is_causal=True)[0].numpy()
+    np.testing.assert_allclose(oracle.sparse_attention(Q, K, V, full, b), ref, rtol=1e-10, atol=1e-12)
+    S = Q @ K.T / math.sqrt(d)
+    for i in range(n):
+        p = np.exp(S[i, : i + 1] - S[i, : i + 1].max())
+        p /= p.sum()
+        a_S = p[E[i, : i + 1]].sum()
+        assert np.all(np.abs(ref[i] - out[i]) <= (1 - a_S) * np.abs(V[: i + 1]).sum(0) + 1e-12)
+
+
+def test_ragged_pipeline_gamma_one_and_min_budget():
+    """gamma = 1 on a ragged generated layer equals dense causal attention (SDPA
+    pin above); forced blocks present; min budget fills rows to min(m, qb + 1)."""
+    from synth import gen
+    from synth.configs import Workload
+    w = Workload("t", 2, 1, 3 * 128 + 45, 1.0, 0.1, 0, 8)
+    q, k, v = gen.make_layer_bits(w)
+    Q, K, V = (gen.bits_to_f64(x) for x in (q, k, v))
+    for h in range(2):
+        r = oracle.flexprefill_head(Q[h], K[0], V[0], 128, 1.0, 0.1, 0)
+        assert r["mask"].sum() == 4 * 5 // 2
+        np.testing.assert_allclose(r["out"], oracle.dense_causal_attention(Q[h], K[0], V[0]),
+                                   rtol=1e-10, atol=1e-12)
+        r = oracle.flexprefill_head(Q[h], K[0], V[0], 128, 0.5, 0.1, 256, with_output=False)
+        for qb in range(4):
+            assert r["mask"][qb, 0] and r["mask"][qb, qb]
+            assert r["mask"][qb].sum() >= min(2, qb + 1)
