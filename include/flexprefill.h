@@ -2,7 +2,7 @@
  * flexprefill.h -- C ABI of libflexprefill.so, a B200 (sm_100a) implementation
  * of FlexPrefill sparse prefill attention (arXiv 2502.20766).
  *
- * Citations: P:n = line n of the paper source; A1..A22 = the
+ * Citations: P:n = line n of the paper source; A1..A26 = the
  * readings of silent/ambiguous passages, listed in DESIGN.md §3.
  *
  * The method (Alg. 1 "Sparse Attention") runs per attention head:
@@ -14,9 +14,14 @@
  *                                                                 -> fp_dense_causal_attn
  *
  * Conventions (all entry points):
- *  - Batch 1, causal, bf16. Q and O are [heads][seq_len][head_dim] row-major,
- *    K and V are [kv_heads][seq_len][head_dim] row-major, contiguous. Q head h
- *    uses KV head floor(h * kv_heads / heads) (GQA, contiguous groups; A15).
+ *  - Causal, bf16. The plain entry points take batch 1 with Q and O
+ *    [heads][seq_len][head_dim] and K, V [kv_heads][seq_len][head_dim],
+ *    row-major, contiguous; the *_ex entry points take an fp_layout (batch >= 1,
+ *    any 16-byte-multiple strides, e.g. the token-major [batch][seq][heads][d]
+ *    of a model's QKV projection). Q head h uses KV head
+ *    floor(h * kv_heads / heads) (GQA, contiguous groups; A15).
+ *  - seq_len is any n >= 128; nb = ceil(n / 128) blocks, the last one ragged
+ *    when n % 128 != 0 (reading A26).
  *  - Every tensor / workspace pointer is a DEVICE pointer unless the name
  *    says host. The caller owns all memory; the library never allocates, keeps
  *    no per-call state, and only enqueues work on `stream` (no host syncs), so
@@ -25,11 +30,13 @@
  *  - Validation is synchronous and happens before anything is enqueued; an
  *    invalid call enqueues nothing and returns a non-zero fp_status:
  *      FP_ERR_NULL      a required pointer is NULL
- *      FP_ERR_SHAPE     heads % kv_heads != 0, seq_len % block_size != 0,
- *                       seq_len < block_size, head_dim != 128, block_size != 128
+ *      FP_ERR_SHAPE     heads % kv_heads != 0, seq_len < block_size,
+ *                       seq_len > 2^20, head_dim != 128, block_size != 128,
+ *                       an fp_layout with batch < 1 or a stride < 128 elements
  *      FP_ERR_RANGE     gamma <= 0 or NaN; tau outside [0,1] or NaN; min_budget < 0
  *                       (gamma >= 1 is allowed and selects every causal block, A7)
- *      FP_ERR_ALIGN     a tensor pointer is not 16-byte aligned (TMA requirement)
+ *      FP_ERR_ALIGN     a tensor pointer is not 16-byte aligned, or an fp_layout
+ *                       stride is not a multiple of 8 elements (TMA requirement)
  *      FP_ERR_WORKSPACE ws_bytes < fp_workspace_bytes(...)
  *      FP_ERR_DEVICE    the current device is not compute capability 10.0
  *      FP_ERR_CUDA      a launch failed; fp_last_cuda_error() has the cudaError_t
@@ -85,9 +92,31 @@ typedef struct {
   int32_t vs_mode, qa_mode, max_budget;
 } fp_select_options;
 
+/* Tensor layout for the *_ex entry points (next row f3). Element (batch b,
+ * head h, position i, dim c) of a tensor lives at
+ *     base + b * stride[0] + h * stride[1] + i * stride[2] + c
+ * (strides in bf16 ELEMENTS, each a multiple of 8 and >= 128; stride[0] is
+ * ignored when batch == 1). K/V head indices run over kv_heads per batch
+ * element, Q/O over heads. With a layout, every per-head array (pattern, jsd,
+ * row_ptr, col_idx, stats, the workspace) covers batch * heads flattened heads
+ * hh = b * heads + h: size the workspace with
+ * fp_workspace_bytes(batch * heads, batch * kv_heads, ...) and call fp_select
+ * with (batch * heads, batch * kv_heads). The caller guarantees that distinct
+ * O rows do not overlap. */
+typedef struct {
+  int32_t batch;
+  int64_t q_stride[3], k_stride[3], v_stride[3], o_stride[3];
+} fp_layout;
+
+/* Contiguous [batch][heads][seq][128] (head-major; the plain entry points'
+ * layout) and [batch][seq][heads][128] (token-major, as produced by a QKV
+ * projection) layouts; host-only helpers, no device work. */
+fp_status fp_layout_bhsd(int batch, int heads, int kv_heads, int seq_len, fp_layout* out);
+fp_status fp_layout_bshd(int batch, int heads, int kv_heads, int seq_len, fp_layout* out);
+
 /* Device pointers into a workspace filled by fp_plan / fp_select (for tests
  * and stage-wise parity; read-only for the caller). Shapes, n = seq_len,
- * nb = n / 128:
+ * nb = ceil(n / 128):
  *   a_v, a_s   fp32 [heads][n]       vertical / slash line scores
  *   a_hat      fp32 [heads][nb]      true block distribution (A2)
  *   a_bar      fp32 [heads][nb]      estimated block distribution
@@ -110,7 +139,7 @@ typedef struct {
  * this shape (0 if the shape is invalid). */
 size_t fp_workspace_bytes(int heads, int kv_heads, int seq_len, int head_dim, int block_size);
 
-/* Per-head capacity (int32 entries) of col_idx: nb * (nb + 1) / 2. */
+/* Per-head capacity (int32 entries) of col_idx: nb * (nb + 1) / 2, nb = ceil(n / 128). */
 size_t fp_col_idx_capacity(int seq_len, int block_size);
 
 /* Stage (i): Alg. 2 for every head, plus the Vertical-Slash line scores of
@@ -126,6 +155,12 @@ size_t fp_col_idx_capacity(int seq_len, int block_size);
 fp_status fp_plan(const void* q, const void* k, int heads, int kv_heads, int seq_len, int head_dim,
                   int block_size, float tau, void* ws, size_t ws_bytes, int32_t* pattern,
                   float* jsd, void* stream);
+
+/* fp_plan over an fp_layout (NULL = the plain layout, batch 1); heads and
+ * kv_heads are per batch element, pattern / jsd are [batch * heads]. */
+fp_status fp_plan_ex(const void* q, const void* k, int heads, int kv_heads, int seq_len,
+                     int head_dim, int block_size, const fp_layout* layout, float tau, void* ws,
+                     size_t ws_bytes, int32_t* pattern, float* jsd, void* stream);
 
 /* Stage (ii): cumulative-attention selection for every head, then
  * forced first/diagonal key blocks (A11) and the minimum budget
@@ -161,10 +196,21 @@ fp_status fp_sparse_attn(const void* q, const void* k, const void* v, void* o, i
                          const int32_t* row_ptr, const int32_t* col_idx, void* ws, size_t ws_bytes,
                          void* stream);
 
+/* fp_sparse_attn over an fp_layout (NULL = plain); row_ptr / col_idx cover the
+ * batch * heads flattened heads. O rows past seq_len are never written. */
+fp_status fp_sparse_attn_ex(const void* q, const void* k, const void* v, void* o, int heads,
+                            int kv_heads, int seq_len, int head_dim, int block_size,
+                            const fp_layout* layout, const int32_t* row_ptr,
+                            const int32_t* col_idx, void* ws, size_t ws_bytes, void* stream);
+
 /* Dense causal attention A(Q, K, V) with the same kernel (every kb <= qb). */
 fp_status fp_dense_causal_attn(const void* q, const void* k, const void* v, void* o, int heads,
                                int kv_heads, int seq_len, int head_dim, int block_size,
                                void* ws, size_t ws_bytes, void* stream);
+fp_status fp_dense_causal_attn_ex(const void* q, const void* k, const void* v, void* o, int heads,
+                                  int kv_heads, int seq_len, int head_dim, int block_size,
+                                  const fp_layout* layout, void* ws, size_t ws_bytes,
+                                  void* stream);
 
 /* The whole layer (Alg. 1) from HOST buffers: copies q/k/v host->device into
  * the caller's device buffers (d_q, d_k, d_v), runs plan/select/attn, and

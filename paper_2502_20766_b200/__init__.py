@@ -18,7 +18,8 @@ import os
 __all__ = [
     "FlexPrefill", "FlexPrefillError", "load_library", "fp_workspace_bytes", "fp_col_idx_capacity",
     "fp_plan", "fp_select", "fp_select_ex", "fp_sparse_attn", "SelectOptions", "fp_dense_causal_attn", "fp_layer_host",
-    "fp_debug_view", "fp_kernels_per_layer", "LIB_PATH", "SelectStats",
+    "fp_debug_view", "fp_kernels_per_layer", "LIB_PATH", "SelectStats", "Layout", "fp_layout_bhsd",
+    "fp_layout_bshd", "fp_plan_ex", "fp_sparse_attn_ex", "fp_dense_causal_attn_ex",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libflexprefill.so")
@@ -52,6 +53,13 @@ class SelectOptions(ctypes.Structure):
                 ("max_budget", ctypes.c_int32)]
 
 
+class Layout(ctypes.Structure):
+    """fp_layout: batch and per-tensor {batch, head, row} strides in elements."""
+    _fields_ = [("batch", ctypes.c_int32), ("q_stride", ctypes.c_int64 * 3),
+                ("k_stride", ctypes.c_int64 * 3), ("v_stride", ctypes.c_int64 * 3),
+                ("o_stride", ctypes.c_int64 * 3)]
+
+
 class DebugPtrs(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "a_v", "a_s", "a_hat", "a_bar", "k_bar", "q_bar", "A_bar", "As",
@@ -83,6 +91,14 @@ def load_library(path=LIB_PATH):
         "fp_layer_host": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _F, _F, _I,
                                _P, _Z, _P, _P, _P, _P, _P]),
         "fp_debug_view": (_I, [_P, _I, _I, _I, _I, _I, ctypes.POINTER(DebugPtrs)]),
+        "fp_layout_bhsd": (_I, [_I, _I, _I, _I, ctypes.POINTER(Layout)]),
+        "fp_layout_bshd": (_I, [_I, _I, _I, _I, ctypes.POINTER(Layout)]),
+        "fp_plan_ex": (_I, [_P, _P, _I, _I, _I, _I, _I, ctypes.POINTER(Layout), _F, _P, _Z, _P, _P,
+                            _P]),
+        "fp_sparse_attn_ex": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.POINTER(Layout), _P,
+                                   _P, _P, _Z, _P]),
+        "fp_dense_causal_attn_ex": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.POINTER(Layout),
+                                         _P, _Z, _P]),
         "fp_kernels_per_layer": (_I, []),
         "fp_status_string": (ctypes.c_char_p, [_I]),
         "fp_last_cuda_error": (_I, []),
@@ -181,6 +197,43 @@ def fp_layer_host(q_host, k_host, v_host, o_host, d_q, d_k, d_v, d_o, heads, kv_
         _stream(stream)))
 
 
+def fp_layout_bhsd(batch, heads, kv_heads, seq_len):
+    lay = Layout()
+    _check("fp_layout_bhsd", _L().fp_layout_bhsd(batch, heads, kv_heads, seq_len, ctypes.byref(lay)))
+    return lay
+
+
+def fp_layout_bshd(batch, heads, kv_heads, seq_len):
+    lay = Layout()
+    _check("fp_layout_bshd", _L().fp_layout_bshd(batch, heads, kv_heads, seq_len, ctypes.byref(lay)))
+    return lay
+
+
+def _lay(layout):
+    return None if layout is None else ctypes.byref(layout)
+
+
+def fp_plan_ex(q, k, heads, kv_heads, seq_len, layout, tau, ws, ws_bytes, pattern, jsd, stream=None,
+               head_dim=128, block_size=128):
+    _check("fp_plan_ex", _L().fp_plan_ex(_ptr(q), _ptr(k), heads, kv_heads, seq_len, head_dim,
+                                         block_size, _lay(layout), tau, _ptr(ws), ws_bytes,
+                                         _ptr(pattern), _ptr(jsd), _stream(stream)))
+
+
+def fp_sparse_attn_ex(q, k, v, o, heads, kv_heads, seq_len, layout, row_ptr, col_idx, ws=None,
+                      ws_bytes=0, stream=None, head_dim=128, block_size=128):
+    _check("fp_sparse_attn_ex", _L().fp_sparse_attn_ex(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(o), heads, kv_heads, seq_len, head_dim, block_size,
+        _lay(layout), _ptr(row_ptr), _ptr(col_idx), _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def fp_dense_causal_attn_ex(q, k, v, o, heads, kv_heads, seq_len, layout, ws=None, ws_bytes=0,
+                            stream=None, head_dim=128, block_size=128):
+    _check("fp_dense_causal_attn_ex", _L().fp_dense_causal_attn_ex(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(o), heads, kv_heads, seq_len, head_dim, block_size,
+        _lay(layout), _ptr(ws), ws_bytes, _stream(stream)))
+
+
 def fp_debug_view(ws, heads, kv_heads, seq_len, head_dim=128, block_size=128):
     d = DebugPtrs()
     _check("fp_debug_view", _L().fp_debug_view(_ptr(ws), heads, kv_heads, seq_len, head_dim,
@@ -190,12 +243,24 @@ def fp_debug_view(ws, heads, kv_heads, seq_len, head_dim=128, block_size=128):
 
 # ------------------------------------------------------------ convenience ---
 class FlexPrefill:
-    """Owns the workspace and CSR buffers for one (heads, kv_heads, seq_len) shape."""
+    """Owns the workspace and CSR buffers for one (heads, kv_heads, seq_len) shape.
 
-    def __init__(self, heads, kv_heads, seq_len, device="cuda"):
+    batch > 1 or layout="bshd" (token-major [batch][seq][heads][128], the
+    layout of a QKV projection) use the *_ex entry points; per-head buffers
+    (pattern, jsd, CSR, stats) then cover batch * heads flattened heads."""
+
+    def __init__(self, heads, kv_heads, seq_len, device="cuda", batch=1, layout="bhsd"):
         import torch
+        if layout not in ("bhsd", "bshd"):
+            raise ValueError(layout)
+        self.heads, self.kv_heads, self.batch = heads, kv_heads, batch
+        self.layout = None
+        if batch != 1 or layout != "bhsd":
+            mk = fp_layout_bhsd if layout == "bhsd" else fp_layout_bshd
+            self.layout = mk(batch, heads, kv_heads, seq_len)
+        heads, kv_heads = batch * heads, batch * kv_heads  # flattened
         self.H, self.G, self.n = heads, kv_heads, seq_len
-        self.nb = seq_len // 128
+        self.nb = -(-seq_len // 128)
         self.ws_bytes = fp_workspace_bytes(heads, kv_heads, seq_len)
         if self.ws_bytes == 0:
             raise FlexPrefillError("fp_workspace_bytes", 2)
@@ -209,6 +274,10 @@ class FlexPrefill:
                                      device=device)
 
     def plan(self, q, k, tau=0.1, stream=None):
+        if self.layout is not None:
+            fp_plan_ex(q, k, self.heads, self.kv_heads, self.n, self.layout, tau, self.ws,
+                       self.ws_bytes, self.pattern, self.jsd, stream)
+            return
         fp_plan(q, k, self.H, self.G, self.n, tau, self.ws, self.ws_bytes, self.pattern, self.jsd,
                 stream)
 
@@ -219,10 +288,18 @@ class FlexPrefill:
                      vs_mode, qa_mode, max_budget)
 
     def attn(self, q, k, v, out, stream=None):
+        if self.layout is not None:
+            fp_sparse_attn_ex(q, k, v, out, self.heads, self.kv_heads, self.n, self.layout,
+                              self.row_ptr, self.col_idx, self.ws, self.ws_bytes, stream)
+            return
         fp_sparse_attn(q, k, v, out, self.H, self.G, self.n, self.row_ptr, self.col_idx, self.ws,
                        self.ws_bytes, stream)
 
     def dense(self, q, k, v, out, stream=None):
+        if self.layout is not None:
+            fp_dense_causal_attn_ex(q, k, v, out, self.heads, self.kv_heads, self.n, self.layout,
+                                    self.ws, self.ws_bytes, stream)
+            return
         fp_dense_causal_attn(q, k, v, out, self.H, self.G, self.n, self.ws, self.ws_bytes, stream)
 
     def layer(self, q, k, v, out, gamma=0.95, tau=0.1, min_budget=0, stream=None):

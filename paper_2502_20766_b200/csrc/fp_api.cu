@@ -25,14 +25,16 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-bool make_tile_map(CUtensorMap* map, const void* base, long long rows) {
+bool make_tile_map(CUtensorMap* map, const void* base, const TLayout& t, int n, int batch) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {128, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {128 * 2};
-  cuuint32_t box[2] = {64, 128};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+  cuuint64_t dims[4] = {128, (cuuint64_t)n, (cuuint64_t)t.per, (cuuint64_t)batch};
+  // batch stride is unused when batch == 1 but must still be a valid value
+  const long long bs = batch > 1 ? t.bs : t.hs * t.per;
+  cuuint64_t strides[3] = {(cuuint64_t)t.rs * 2, (cuuint64_t)t.hs * 2, (cuuint64_t)bs * 2};
+  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -42,8 +44,31 @@ static fp_status check_shape(int heads, int kv_heads, int seq_len, int head_dim,
   if (heads <= 0 || kv_heads <= 0 || seq_len <= 0) return FP_ERR_SHAPE;
   if (heads % kv_heads != 0) return FP_ERR_SHAPE;
   if (head_dim != 128 || block_size != 128) return FP_ERR_SHAPE;
-  if (seq_len % block_size != 0 || seq_len < block_size) return FP_ERR_SHAPE;
+  if (seq_len < block_size) return FP_ERR_SHAPE;  // ragged n allowed (A26), n >= b (A13)
   if (seq_len > (1 << 20)) return FP_ERR_SHAPE;  // bitmap / index capacity limit
+  return FP_OK;
+}
+
+// fp_layout -> internal Layout (validated); NULL = [heads][n][128] contiguous, batch 1
+static fp_status to_layout(const fp_layout* in, int heads, int kv_heads, int seq_len, Layout* out) {
+  if (!in) {
+    *out = head_major_layout(1, heads, kv_heads, seq_len);
+    return FP_OK;
+  }
+  if (in->batch < 1 || (long long)in->batch * heads > (1 << 24)) return FP_ERR_SHAPE;
+  const int64_t* st[4] = {in->q_stride, in->k_stride, in->v_stride, in->o_stride};
+  TLayout* t[4] = {&out->q, &out->k, &out->v, &out->o};
+  for (int i = 0; i < 4; ++i) {
+    for (int j = 0; j < 3; ++j) {
+      if (j == 0 && in->batch == 1) continue;  // unused
+      if (st[i][j] < 128 || st[i][j] >= (1ll << 38)) return FP_ERR_SHAPE;
+      if (st[i][j] % 8) return FP_ERR_ALIGN;  // TMA: 16-byte global strides
+    }
+    const int per = (i == 1 || i == 2) ? kv_heads : heads;
+    const long long bs = in->batch == 1 ? st[i][1] * per : st[i][0];
+    *t[i] = TLayout{bs, st[i][1], st[i][2], per};
+  }
+  out->batch = in->batch;
   return FP_OK;
 }
 
@@ -76,9 +101,36 @@ size_t fp_workspace_bytes(int heads, int kv_heads, int seq_len, int head_dim, in
   return ws_layout(make_shape(heads, kv_heads, seq_len)).total;
 }
 
+fp_status fp_layout_bhsd(int batch, int heads, int kv_heads, int seq_len, fp_layout* out) {
+  if (!out) return FP_ERR_NULL;
+  if (batch < 1 || heads <= 0 || kv_heads <= 0 || seq_len <= 0) return FP_ERR_SHAPE;
+  const int64_t n = seq_len;
+  const int64_t q[3] = {heads * n * 128, n * 128, 128}, k[3] = {kv_heads * n * 128, n * 128, 128};
+  out->batch = batch;
+  memcpy(out->q_stride, q, sizeof q);
+  memcpy(out->o_stride, q, sizeof q);
+  memcpy(out->k_stride, k, sizeof k);
+  memcpy(out->v_stride, k, sizeof k);
+  return FP_OK;
+}
+
+fp_status fp_layout_bshd(int batch, int heads, int kv_heads, int seq_len, fp_layout* out) {
+  if (!out) return FP_ERR_NULL;
+  if (batch < 1 || heads <= 0 || kv_heads <= 0 || seq_len <= 0) return FP_ERR_SHAPE;
+  const int64_t n = seq_len;
+  const int64_t q[3] = {n * heads * 128, 128, (int64_t)heads * 128};
+  const int64_t k[3] = {n * kv_heads * 128, 128, (int64_t)kv_heads * 128};
+  out->batch = batch;
+  memcpy(out->q_stride, q, sizeof q);
+  memcpy(out->o_stride, q, sizeof q);
+  memcpy(out->k_stride, k, sizeof k);
+  memcpy(out->v_stride, k, sizeof k);
+  return FP_OK;
+}
+
 size_t fp_col_idx_capacity(int seq_len, int block_size) {
   if (block_size <= 0 || seq_len <= 0) return 0;
-  const size_t nb = (size_t)seq_len / block_size;
+  const size_t nb = ((size_t)seq_len + block_size - 1) / block_size;
   return nb * (nb + 1) / 2;
 }
 
@@ -87,20 +139,29 @@ int fp_kernels_per_layer(void) { return 9 + 6 + 1; }
 fp_status fp_plan(const void* q, const void* k, int heads, int kv_heads, int seq_len, int head_dim,
                   int block_size, float tau, void* ws, size_t ws_bytes, int32_t* pattern,
                   float* jsd, void* stream) {
+  return fp_plan_ex(q, k, heads, kv_heads, seq_len, head_dim, block_size, nullptr, tau, ws, ws_bytes,
+                    pattern, jsd, stream);
+}
+
+fp_status fp_plan_ex(const void* q, const void* k, int heads, int kv_heads, int seq_len,
+                     int head_dim, int block_size, const fp_layout* layout, float tau, void* ws,
+                     size_t ws_bytes, int32_t* pattern, float* jsd, void* stream) {
   if (!q || !k || !ws) return FP_ERR_NULL;
   fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
   if (st) return st;
   if (!(tau >= 0.f && tau <= 1.f)) return FP_ERR_RANGE;
+  Layout lay;
+  if ((st = to_layout(layout, heads, kv_heads, seq_len, &lay))) return st;
   if (!aligned16(q) || !aligned16(k) || !aligned16(ws)) return FP_ERR_ALIGN;
-  const Shape s = make_shape(heads, kv_heads, seq_len);
+  const Shape s = make_shape(lay.batch * heads, lay.batch * kv_heads, seq_len);
   const WsLayout L = ws_layout(s);
   if (ws_bytes < L.total) return FP_ERR_WORKSPACE;
   if ((st = check_device())) return st;
   CUtensorMap qm, km;
-  if (!make_tile_map(&qm, q, (long long)heads * seq_len) ||
-      !make_tile_map(&km, k, (long long)kv_heads * seq_len))
+  if (!make_tile_map(&qm, q, lay.q, seq_len, lay.batch) ||
+      !make_tile_map(&km, k, lay.k, seq_len, lay.batch))
     return cuda_status(cudaErrorInvalidValue);
-  return cuda_status(launch_plan(s, L, ws, q, k, qm, km, tau, pattern, jsd,
+  return cuda_status(launch_plan(s, L, ws, q, k, lay, qm, km, tau, pattern, jsd,
                                  static_cast<cudaStream_t>(stream)));
 }
 
@@ -134,23 +195,26 @@ fp_status fp_select_ex(int heads, int kv_heads, int seq_len, int head_dim, int b
 
 static fp_status attn_common(const void* q, const void* k, const void* v, void* o, int heads,
                              int kv_heads, int seq_len, int head_dim, int block_size,
-                             const int32_t* row_ptr, const int32_t* col_idx, void* ws,
-                             size_t ws_bytes, void* stream, bool dense) {
+                             const fp_layout* layout, const int32_t* row_ptr,
+                             const int32_t* col_idx, void* ws, size_t ws_bytes, void* stream,
+                             bool dense) {
   if (!q || !k || !v || !o) return FP_ERR_NULL;
   if (!dense && (!row_ptr || !col_idx)) return FP_ERR_NULL;
   fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
   if (st) return st;
+  Layout lay;
+  if ((st = to_layout(layout, heads, kv_heads, seq_len, &lay))) return st;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return FP_ERR_ALIGN;
   (void)ws_bytes;
   if ((st = check_device())) return st;
-  const Shape s = make_shape(heads, kv_heads, seq_len);
+  const Shape s = make_shape(lay.batch * heads, lay.batch * kv_heads, seq_len);
   const WsLayout L = ws_layout(s);
   CUtensorMap qm, km, vm;
-  if (!make_tile_map(&qm, q, (long long)heads * seq_len) ||
-      !make_tile_map(&km, k, (long long)kv_heads * seq_len) ||
-      !make_tile_map(&vm, v, (long long)kv_heads * seq_len))
+  if (!make_tile_map(&qm, q, lay.q, seq_len, lay.batch) ||
+      !make_tile_map(&km, k, lay.k, seq_len, lay.batch) ||
+      !make_tile_map(&vm, v, lay.v, seq_len, lay.batch))
     return cuda_status(cudaErrorInvalidValue);
-  return cuda_status(launch_attn(s, L, ws, qm, km, vm, o, row_ptr, col_idx, dense,
+  return cuda_status(launch_attn(s, L, ws, lay, qm, km, vm, o, row_ptr, col_idx, dense,
                                  static_cast<cudaStream_t>(stream)));
 }
 
@@ -158,15 +222,31 @@ fp_status fp_sparse_attn(const void* q, const void* k, const void* v, void* o, i
                          int kv_heads, int seq_len, int head_dim, int block_size,
                          const int32_t* row_ptr, const int32_t* col_idx, void* ws, size_t ws_bytes,
                          void* stream) {
-  return attn_common(q, k, v, o, heads, kv_heads, seq_len, head_dim, block_size, row_ptr, col_idx,
-                     ws, ws_bytes, stream, false);
+  return attn_common(q, k, v, o, heads, kv_heads, seq_len, head_dim, block_size, nullptr, row_ptr,
+                     col_idx, ws, ws_bytes, stream, false);
+}
+
+fp_status fp_sparse_attn_ex(const void* q, const void* k, const void* v, void* o, int heads,
+                            int kv_heads, int seq_len, int head_dim, int block_size,
+                            const fp_layout* layout, const int32_t* row_ptr,
+                            const int32_t* col_idx, void* ws, size_t ws_bytes, void* stream) {
+  return attn_common(q, k, v, o, heads, kv_heads, seq_len, head_dim, block_size, layout, row_ptr,
+                     col_idx, ws, ws_bytes, stream, false);
 }
 
 fp_status fp_dense_causal_attn(const void* q, const void* k, const void* v, void* o, int heads,
                                int kv_heads, int seq_len, int head_dim, int block_size, void* ws,
                                size_t ws_bytes, void* stream) {
   return attn_common(q, k, v, o, heads, kv_heads, seq_len, head_dim, block_size, nullptr, nullptr,
-                     ws, ws_bytes, stream, true);
+                     nullptr, ws, ws_bytes, stream, true);
+}
+
+fp_status fp_dense_causal_attn_ex(const void* q, const void* k, const void* v, void* o, int heads,
+                                  int kv_heads, int seq_len, int head_dim, int block_size,
+                                  const fp_layout* layout, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  return attn_common(q, k, v, o, heads, kv_heads, seq_len, head_dim, block_size, layout, nullptr,
+                     nullptr, ws, ws_bytes, stream, true);
 }
 
 fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_host, void* o_host,
@@ -190,7 +270,7 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
   // two workspace slots (the full-layer workspace holds at least two).
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   const int g = heads / kv_heads;
-  const size_t n = (size_t)seq_len, nb = n / 128, cap = nb * (nb + 1) / 2;
+  const size_t n = (size_t)seq_len, nb = (n + 127) / 128, cap = nb * (nb + 1) / 2;
   const size_t qb_bytes = (size_t)g * n * 128 * 2, kv_bytes = n * 128 * 2;
   const size_t slot = align256(fp_workspace_bytes(g, 1, seq_len, head_dim, block_size));
   const int nslots = (kv_heads > 1 && ws_bytes >= 2 * slot) ? 2 : 1;

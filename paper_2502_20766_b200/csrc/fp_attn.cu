@@ -216,8 +216,9 @@ FP_DEV void softmax_tile(float* v, int R0, int a, float scale_log2, float* m_use
 template <bool DENSE>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-                const __grid_constant__ CUtensorMap vmap, __nv_bfloat16* __restrict__ o, int H,
-                int G, int n, int nb, long long cap, const int32_t* __restrict__ row_ptr,
+                const __grid_constant__ CUtensorMap vmap, __nv_bfloat16* __restrict__ o,
+                const TLayout ol, int Hp, int Gp, int H, int G, int n, int nb, long long cap,
+                const int32_t* __restrict__ row_ptr,
                 const int32_t* __restrict__ col_idx, float scale_log2) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // the 7 SW128 tiles fill 224 KiB: no room for alignment slack. The dynamic
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint64_t pol_kv = policy_evict_last();
       if (isK) {
         mbar_arrive_expect_tx(&sm.q_full, kTileBytes);
-        tma_load_tile(sm.q, &qmap, &sm.q_full, h * n + qb * 128);
+        tma_tile(sm.q, &qmap, &sm.q_full, qb * 128, h, Hp);
       }
       uint64_t* full = isK ? sm.k_full : sm.v_full;
       uint64_t* empty = isK ? sm.k_empty : sm.v_empty;
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int kb = DENSE ? i : __ldg(list + i);
         if (i >= kKV) mbar_wait(&empty[s], ((i - kKV) / kKV) & 1);
         mbar_arrive_expect_tx(&full[s], kTileBytes);
-        tma_load_tile_hint(isK ? sm.k[s] : sm.v[s], map, &full[s], g * n + kb * 128, pol_kv);
+        tma_tile_hint(isK ? sm.k[s] : sm.v[s], map, &full[s], kb * 128, g, Gp, pol_kv);
       }
     }
   } else if (wid == 9) {
@@ -425,12 +426,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     float ov[64];
     tmem_ld_16x256b_x16(tO, reinterpret_cast<uint32_t*>(ov));
     tmem_wait_ld();
-    uint32_t* d0 = reinterpret_cast<uint32_t*>(o + ((size_t)h * n + (size_t)qb * 128 + R0) * 128) + a;
-    uint32_t* d1 = d0 + 8 * 64;  // row R0 + 8 (64 bf16 pairs per row)
+    // rows past n (ragged last block, zero-filled Q) are not stored
+    const int row0 = qb * 128 + R0;
+    uint32_t* d0 = reinterpret_cast<uint32_t*>(o + toff(ol, h, row0)) + a;
+    uint32_t* d1 = d0 + 4 * ol.rs;  // row R0 + 8 (rs elements = rs / 2 bf16 pairs per row)
+    if (row0 < n) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      d0[4 * k] = pack_bf16x2(ov[4 * k] * il0, ov[4 * k + 1] * il0);
-      d1[4 * k] = pack_bf16x2(ov[4 * k + 2] * il1, ov[4 * k + 3] * il1);
+      for (int k = 0; k < 16; ++k) d0[4 * k] = pack_bf16x2(ov[4 * k] * il0, ov[4 * k + 1] * il0);
+    }
+    if (row0 + 8 < n) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) d1[4 * k] = pack_bf16x2(ov[4 * k + 2] * il1, ov[4 * k + 3] * il1);
     }
   }
   tc_fence_before();
@@ -442,8 +448,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
 size_t attn_smem_bytes() { return sizeof(AttnSmem); }
 
-cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const CUtensorMap& qmap,
-                        const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layout& lay,
+                        const CUtensorMap& qmap, const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                         const int32_t* row_ptr, const int32_t* col_idx, bool dense,
                         cudaStream_t st) {
   (void)L;
@@ -459,13 +465,13 @@ cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const CUten
   const dim3 grid(s.H * s.nb);
   if (dense)
     attn_kernel<true><<<grid, kAttnThreads, smem, st>>>(qmap, kmap, vmap,
-                                                        reinterpret_cast<__nv_bfloat16*>(o), s.H,
-                                                        s.G, s.n, s.nb, s.tri, row_ptr, col_idx,
+                                                        reinterpret_cast<__nv_bfloat16*>(o), lay.o,
+                                                        lay.q.per, lay.k.per, s.H, s.G, s.n, s.nb, s.tri, row_ptr, col_idx,
                                                         scale_log2);
   else
     attn_kernel<false><<<grid, kAttnThreads, smem, st>>>(qmap, kmap, vmap,
-                                                         reinterpret_cast<__nv_bfloat16*>(o), s.H,
-                                                         s.G, s.n, s.nb, s.tri, row_ptr, col_idx,
+                                                         reinterpret_cast<__nv_bfloat16*>(o), lay.o,
+                                                         lay.q.per, lay.k.per, s.H, s.G, s.n, s.nb, s.tri, row_ptr, col_idx,
                                                          scale_log2);
   return cudaGetLastError();
 }

@@ -102,6 +102,43 @@ FP_DEV uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// 4D tile loads: tensor {128 cols, rows, heads, batch} (fp_api.cu make_tile_map);
+// rows past the end of a sequence are zero-filled by the TMA unit.
+FP_DEV void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                        int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+FP_DEV void tma_load_4d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                             int c2, int c3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "l"(policy)
+      : "memory");
+}
+// Flattened head index hh = batch * per + head  ->  (head, batch) coordinates.
+struct HeadCoord {
+  int h, b;
+};
+FP_DEV HeadCoord head_coord(int hh, int per) { return HeadCoord{hh % per, hh / per}; }
+// 128 x 128 tile of rows [row, row + 128) of flattened head hh (two SW128 boxes).
+FP_DEV void tma_tile(void* dst, const CUtensorMap* m, uint64_t* bar, int row, int hh, int per) {
+  const HeadCoord c = head_coord(hh, per);
+  tma_load_4d(dst, m, bar, 0, row, c.h, c.b);
+  tma_load_4d(static_cast<char*>(dst) + kBoxBytes, m, bar, 64, row, c.h, c.b);
+}
+FP_DEV void tma_tile_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int row, int hh, int per,
+                          uint64_t pol) {
+  const HeadCoord c = head_coord(hh, per);
+  tma_load_4d_hint(dst, m, bar, 0, row, c.h, c.b, pol);
+  tma_load_4d_hint(static_cast<char*>(dst) + kBoxBytes, m, bar, 64, row, c.h, c.b, pol);
+}
+
 // Load a full 128-row x 128-col bf16 tile as two 128x64 SW128 boxes.
 FP_DEV void tma_load_tile(void* dst, const CUtensorMap* m, uint64_t* bar, int row) {
   tma_load_2d(dst, m, bar, 0, row);

@@ -12,7 +12,7 @@ namespace fp {
 constexpr int kChunkTilesMax = 8;  // key tiles (128 keys) per representative-pass CTA (max)
 
 struct Shape {
-  int H, G, n, nb, nchunks, g;  // g = H / G
+  int H, G, n, nb, nchunks, g;  // flattened heads (batch * heads per sequence); g = H / G
   int ct;                       // key tiles per representative-pass CTA
   long long tri;                // nb (nb + 1) / 2
 };
@@ -22,7 +22,7 @@ inline Shape make_shape(int heads, int kv_heads, int seq_len) {
   s.H = heads;
   s.G = kv_heads;
   s.n = seq_len;
-  s.nb = seq_len / 128;
+  s.nb = (seq_len + 127) / 128;  // ragged n: the last block is partial (A26)
   // largest chunk (<= 8 tiles) that still gives >= 2 CTAs per SM of the
   // 148-SM B200 for the representative passes (short sequences: smaller chunks)
   s.ct = kChunkTilesMax;
@@ -105,23 +105,52 @@ inline WsLayout ws_layout(const Shape& s) {
   return L;
 }
 
+// Element (flattened head hh, position i, dim c) of a Q/K/V/O tensor lives at
+// base + (hh / per) * bs + (hh % per) * hs + i * rs + c  (all in elements).
+struct TLayout {
+  long long bs, hs, rs;
+  int per;  // heads per batch element
+};
+struct Layout {
+  TLayout q, k, v, o;
+  int batch;
+};
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline size_t toff(const TLayout& t, int hh, int i) {
+  return (size_t)(hh / t.per) * (size_t)t.bs + (size_t)(hh % t.per) * (size_t)t.hs +
+         (size_t)i * (size_t)t.rs;
+}
+// [batch][heads][n][128] contiguous (the default of the plain entry points)
+inline Layout head_major_layout(int batch, int heads, int kv_heads, int n) {
+  Layout L;
+  L.batch = batch;
+  L.q = TLayout{(long long)heads * n * 128, (long long)n * 128, 128, heads};
+  L.k = TLayout{(long long)kv_heads * n * 128, (long long)n * 128, 128, kv_heads};
+  L.v = L.k;
+  L.o = L.q;
+  return L;
+}
+
 template <typename T>
 inline T* wsp(void* ws, size_t off) {
   return reinterpret_cast<T*>(static_cast<char*>(ws) + off);
 }
 
-// 2D bf16 tensor map: rows x 128 columns, box 128 rows x 64 cols, SWIZZLE_128B.
-bool make_tile_map(CUtensorMap* map, const void* base, long long rows);
+// 4D bf16 tensor map {128 cols, n rows, per heads, batch} with the strides of
+// `t`; box 64 cols x 128 rows, SWIZZLE_128B; rows >= n are zero-filled.
+bool make_tile_map(CUtensorMap* map, const void* base, const TLayout& t, int n, int batch);
 
 // ---- launchers (return cudaGetLastError of their launches) ----
 cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void* q, const void* k,
-                        const CUtensorMap& qmap, const CUtensorMap& kmap, float tau,
+                        const Layout& lay, const CUtensorMap& qmap, const CUtensorMap& kmap, float tau,
                         int32_t* pattern_out, float* jsd_out, cudaStream_t st);
 cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gamma, int min_budget,
                           const fp_select_options& opt, int32_t* row_ptr, int32_t* col_idx,
                           fp_select_stats* stats, cudaStream_t st);
-cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const CUtensorMap& qmap,
-                        const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layout& lay,
+                        const CUtensorMap& qmap, const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                         const int32_t* row_ptr, const int32_t* col_idx, bool dense,
                         cudaStream_t st);
 

@@ -108,7 +108,8 @@ __device__ float block_max(float v, float* red) {
 template <int PASS>
 __global__ void __launch_bounds__(kRepThreads, 1)
     rep_pass(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-             int H, int G, int n, int nb, int nchunks, int ct, float scale_log2, float* __restrict__ m_part,
+             int H, int G, int Hp, int Gp, int n, int nb, int nchunks, int ct, float scale_log2,
+             float* __restrict__ m_part,
              float* __restrict__ l_part, const float* __restrict__ m_row,
              const float* __restrict__ il_row, float* __restrict__ k_bar, float* __restrict__ a_v,
              float* __restrict__ as_part) {
@@ -162,10 +163,10 @@ __global__ void __launch_bounds__(kRepThreads, 1)
 
   if (tid == 0) {
     mbar_arrive_expect_tx(&sm.q_full, kTileBytes);
-    tma_load_tile(sm.qhat, &qmap, &sm.q_full, h * n + n - 128);
+    tma_tile(sm.qhat, &qmap, &sm.q_full, n - 128, h, Hp);
     for (int s = 0; s < kStages && s < ntile; ++s) {
       mbar_arrive_expect_tx(&sm.k_full[s], kTileBytes);
-      tma_load_tile(sm.kst[s], &kmap, &sm.k_full[s], g * n + (t0 + s) * 128);
+      tma_tile(sm.kst[s], &kmap, &sm.k_full[s], (t0 + s) * 128, g, Gp);
     }
     mbar_wait(&sm.q_full, 0);
     issue_mma(0);
@@ -177,7 +178,10 @@ __global__ void __launch_bounds__(kRepThreads, 1)
     if (tid == 0 && t + 1 < ntile) issue_mma(t + 1);
     const int b = t & 1;
     const int tile = t0 + t;
-    const bool last = (tile == nb - 1);
+    // key tile*128 + c is visible from rep row r iff c <= lim + r (p_r = n-128+r);
+    // only the last one or two tiles (ragged n) need the mask
+    const int lim = n - 128 - tile * 128;
+    const bool last = lim < 127;
     mbar_wait(&sm.mma_done[b], (t >> 1) & 1);
     tc_fence_after();
 
@@ -194,12 +198,12 @@ __global__ void __launch_bounds__(kRepThreads, 1)
 #pragma unroll
       for (int c = 0; c < 64; ++c) {
         float x = __uint_as_float(v[c]) * scale_log2;
-        if (last && half * 64 + c > r) x = -INFINITY;
+        if (last && half * 64 + c > lim + r) x = -INFINITY;
         v[c] = __float_as_uint(x);
         mx4[c & 3] = fmaxf(mx4[c & 3], x);
       }
       const float m_new = fmaxf(m_loc, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
-      // a column half can be fully masked (last tile, rows < 64): keep it at -inf, sum 0
+      // a column half can be fully masked (last tiles): keep it at -inf, sum 0
       const float m_safe = (m_new == -INFINITY) ? 0.f : m_new;
       float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -218,8 +222,10 @@ __global__ void __launch_bounds__(kRepThreads, 1)
         }
         sm.red[tid] = a0 + a1;
         __syncthreads();
+        // ragged last block: zero-filled rows past n, mean over the actual rows (A26)
         if (tid < 128)
-          k_bar[((size_t)g * nb + tile) * 128 + tid] = (sm.red[tid] + sm.red[tid + 128]) * (1.0f / 128.0f);
+          k_bar[((size_t)g * nb + tile) * 128 + tid] =
+              (sm.red[tid] + sm.red[tid + 128]) / (float)min(128, n - tile * 128);
       }
     } else {
       // lane = key j_local, columns = rep rows r = half*64 .. half*64+63
@@ -231,13 +237,14 @@ __global__ void __launch_bounds__(kRepThreads, 1)
       for (int c = 0; c < 64; ++c) {
         const int r = half * 64 + c;
         float p = fast_exp2(fmaf(__uint_as_float(v[c]), scale_log2, -sm.m_row[r])) * sm.il_row[r];
-        if (last && jl > r) p = 0.f;
+        if (last && jl > lim + r) p = 0.f;
         cs[c & 3] += p;
         Trow[c] = p;
       }
       sm.red[half * 128 + jl] = (cs[0] + cs[1]) + (cs[2] + cs[3]);
       __syncthreads();
-      if (tid < 128) a_v[(size_t)h * n + tile * 128 + tid] = (sm.red[tid] + sm.red[128 + tid]) * (1.0f / 128.0f);
+      if (tid < 128 && tile * 128 + tid < n)
+        a_v[(size_t)h * n + tile * 128 + tid] = (sm.red[tid] + sm.red[128 + tid]) * (1.0f / 128.0f);
       (void)j;
       // slash partials: diagonal delta = r - jl in [-127, 127], one per thread;
       // offset o = p_r - j = (n - 128 - tile*128) + delta
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(kRepThreads, 1)
     if (tid == 0 && t + kStages < ntile) {
       const int s = t % kStages;
       mbar_arrive_expect_tx(&sm.k_full[s], kTileBytes);
-      tma_load_tile(sm.kst[s], &kmap, &sm.k_full[s], g * n + (t0 + t + kStages) * 128);
+      tma_tile(sm.kst[s], &kmap, &sm.k_full[s], (t0 + t + kStages) * 128, g, Gp);
     }
   }
 
@@ -274,7 +281,9 @@ __global__ void __launch_bounds__(kRepThreads, 1)
     if (tid < 128) {
       const float m0 = sm.red[tid], m1 = sm.red[tid + 128];
       const float m = fmaxf(m0, m1);
-      const float l = sm.red[256 + tid] * fast_exp2(m0 - m) + sm.red[256 + tid + 128] * fast_exp2(m1 - m);
+      // ragged n: a whole chunk can be invisible to a row (m = -inf, l = 0)
+      const float ms = (m == -INFINITY) ? 0.f : m;
+      const float l = sm.red[256 + tid] * fast_exp2(m0 - ms) + sm.red[256 + tid + 128] * fast_exp2(m1 - ms);
       m_part[((size_t)h * nchunks + chunk) * 128 + tid] = m;
       l_part[((size_t)h * nchunks + chunk) * 128 + tid] = l;
     }
@@ -324,8 +333,9 @@ __global__ void block_sums(int n, int nb, const float* __restrict__ a_v,
   __shared__ float red[33];
   const int kb = blockIdx.x, h = blockIdx.y;
   const size_t i = (size_t)h * n + (size_t)kb * 128 + threadIdx.x;
-  float sv = block_sum<128>(a_v[i], red);
-  float ss = block_sum<128>(a_s[i], red);
+  const bool in = kb * 128 + (int)threadIdx.x < n;  // ragged last block (A26)
+  float sv = block_sum<128>(in ? a_v[i] : 0.f, red);
+  float ss = block_sum<128>(in ? a_s[i] : 0.f, red);
   if (threadIdx.x == 0) {
     a_hat[(size_t)h * nb + kb] = sv;
     As[(size_t)h * nb + kb] = ss;
@@ -335,7 +345,7 @@ __global__ void block_sums(int n, int nb, const float* __restrict__ a_v,
 // Alg. 2: a_bar, D_JS (base 2, A1), decision (strict <, A14)
 constexpr int kPatThreads = 256;
 __global__ void __launch_bounds__(kPatThreads) pattern_kernel(
-    const __nv_bfloat16* __restrict__ q, const float* __restrict__ k_bar,
+    const __nv_bfloat16* __restrict__ q, TLayout ql, const float* __restrict__ k_bar,
     const float* __restrict__ a_hat, int H, int G, int n, int nb, float scale, float tau,
     float* __restrict__ a_bar, int32_t* __restrict__ pattern_ws, float* __restrict__ jsd_ws,
     int32_t* __restrict__ pattern_out, float* __restrict__ jsd_out) {
@@ -346,9 +356,9 @@ __global__ void __launch_bounds__(kPatThreads) pattern_kernel(
   const int h = blockIdx.x, g = h / (H / G);
   const int tid = threadIdx.x;
   if (tid < 128) {
-    const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + ((size_t)h * n + n - 128) * 128;
+    const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + toff(ql, h, n - 128) + tid;
     float acc = 0.f;
-    for (int r = 0; r < 128; ++r) acc += bf16_to_f32(qh[r * 128 + tid]);
+    for (int r = 0; r < 128; ++r) acc += bf16_to_f32(qh[(size_t)r * ql.rs]);
     qbar[tid] = acc * (1.0f / 128.0f);
   }
   __syncthreads();
@@ -390,15 +400,18 @@ __global__ void __launch_bounds__(kPatThreads) pattern_kernel(
 }
 
 // avg-pooled queries of Query-Aware heads (Alg. 4 line 1)
-__global__ void qbar_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pattern,
-                            int n, int nb, float* __restrict__ q_bar) {
+// (a ragged last block averages over its actual rows, A26)
+__global__ void qbar_kernel(const __nv_bfloat16* __restrict__ q, TLayout ql,
+                            const int32_t* __restrict__ pattern, int n, int nb,
+                            float* __restrict__ q_bar) {
   const int qb = blockIdx.x, h = blockIdx.y;
   if (pattern[h] != 1) return;
-  const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + ((size_t)h * n + (size_t)qb * 128) * 128;
+  const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + toff(ql, h, qb * 128) + threadIdx.x;
+  const int cnt = min(128, n - qb * 128);
   float acc = 0.f;
 #pragma unroll 8
-  for (int r = 0; r < 128; ++r) acc += bf16_to_f32(qh[r * 128 + threadIdx.x]);
-  q_bar[((size_t)h * nb + qb) * 128 + threadIdx.x] = acc * (1.0f / 128.0f);
+  for (int r = 0; r < cnt; ++r) acc += bf16_to_f32(qh[(size_t)r * ql.rs]);
+  q_bar[((size_t)h * nb + qb) * 128 + threadIdx.x] = acc / (float)cnt;
 }
 
 // A_bar[qb, kb <= qb] = softmax_row(scale * Qbar[qb] . Kbar[kb]) / nb  (A5)
@@ -469,7 +482,7 @@ size_t rep_smem_bytes(int pass) {
 }
 
 cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void* q, const void* k,
-                        const CUtensorMap& qmap, const CUtensorMap& kmap, float tau,
+                        const Layout& lay, const CUtensorMap& qmap, const CUtensorMap& kmap, float tau,
                         int32_t* pattern_out, float* jsd_out, cudaStream_t st) {
   static bool attr_done = false;
   const size_t sm1 = rep_smem_bytes(1), sm2 = rep_smem_bytes(2);
@@ -485,12 +498,14 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
   float* m_row = wsp<float>(ws, L.m_row);
   float* il_row = wsp<float>(ws, L.il_row);
   dim3 grid(s.nchunks, s.H);
-  rep_pass<1><<<grid, kRepThreads, sm1, st>>>(qmap, kmap, s.H, s.G, s.n, s.nb, s.nchunks, s.ct, scale_log2,
+  (void)k;
+  const int Hp = lay.q.per, Gp = lay.k.per;
+  rep_pass<1><<<grid, kRepThreads, sm1, st>>>(qmap, kmap, s.H, s.G, Hp, Gp, s.n, s.nb, s.nchunks, s.ct, scale_log2,
                                               m_part, l_part, m_row, il_row,
                                               wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_v),
                                               wsp<float>(ws, L.as_part));
   rep_stats<<<s.H, 128, 0, st>>>(s.nchunks, m_part, l_part, m_row, il_row);
-  rep_pass<2><<<grid, kRepThreads, sm2, st>>>(qmap, kmap, s.H, s.G, s.n, s.nb, s.nchunks, s.ct, scale_log2,
+  rep_pass<2><<<grid, kRepThreads, sm2, st>>>(qmap, kmap, s.H, s.G, Hp, Gp, s.n, s.nb, s.nchunks, s.ct, scale_log2,
                                               m_part, l_part, m_row, il_row,
                                               wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_v),
                                               wsp<float>(ws, L.as_part));
@@ -501,10 +516,10 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
                                               wsp<float>(ws, L.As));
   const size_t psm = (128 + (size_t)s.nb + 33) * 4;
   pattern_kernel<<<s.H, kPatThreads, psm, st>>>(
-      reinterpret_cast<const __nv_bfloat16*>(q), wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_hat),
+      reinterpret_cast<const __nv_bfloat16*>(q), lay.q, wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_hat),
       s.H, s.G, s.n, s.nb, scale, tau, wsp<float>(ws, L.a_bar), wsp<int32_t>(ws, L.pattern),
       wsp<float>(ws, L.jsd), pattern_out, jsd_out);
-  qbar_kernel<<<dim3(s.nb, s.H), 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(q),
+  qbar_kernel<<<dim3(s.nb, s.H), 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
                                                wsp<int32_t>(ws, L.pattern), s.n, s.nb,
                                                wsp<float>(ws, L.q_bar));
   const int nt = (s.nb + kPT - 1) / kPT;

@@ -116,7 +116,7 @@ def stagewise_mask(pattern, dbg, h, n, gamma, min_budget, b=128, vs_mode=0, qa_m
     The budget orders are decided in fp32 like the kernel (A12 score
     a_hat[kb] + As[qb-kb] rounded to fp32; QA: A_bar in fp32). For the
     per-row QA mode the oracle's per-row topmass runs on the GPU's fp32 A_bar."""
-    nb = n // b
+    nb = -(-n // b)  # ragged n (A26)
     cnt = dbg["sel_count"][h]
     if pattern == oracle.VS:
         S_v = dbg["sel_v"][h, : cnt[0]]

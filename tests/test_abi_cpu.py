@@ -40,7 +40,7 @@ def test_workspace_and_capacity(lib):
     b1 = fp.fp_workspace_bytes(32, 8, 32768)
     b2 = fp.fp_workspace_bytes(32, 8, 131072)
     assert 0 < b1 < b2 < (1 << 31)
-    for bad in [(32, 7, 32768), (32, 8, 1000), (32, 8, 64), (0, 1, 2048)]:
+    for bad in [(32, 7, 32768), (32, 8, 100), (32, 8, 64), (0, 1, 2048)]:
         assert fp.fp_workspace_bytes(*bad) == 0
     assert fp.fp_workspace_bytes(4, 1, 2048, head_dim=64) == 0
     assert fp.fp_workspace_bytes(4, 1, 2048, block_size=64) == 0
@@ -53,7 +53,8 @@ def test_validation_codes_without_device(lib):
     s = ctypes.c_void_p(0)
     assert L.fp_plan(None, P, 4, 1, 2048, 128, 128, 0.1, P, ws_bytes, P, P, s) == 1
     assert L.fp_plan(P, P, 4, 3, 2048, 128, 128, 0.1, P, ws_bytes, P, P, s) == 2
-    assert L.fp_plan(P, P, 4, 1, 2000, 128, 128, 0.1, P, ws_bytes, P, P, s) == 2
+    assert L.fp_plan(P, P, 4, 1, 127, 128, 128, 0.1, P, ws_bytes, P, P, s) == 2
+    assert L.fp_plan(P, P, 4, 1, (1 << 20) + 128, 128, 128, 0.1, P, ws_bytes, P, P, s) == 2
     assert L.fp_plan(P, P, 4, 1, 2048, 64, 128, 0.1, P, ws_bytes, P, P, s) == 2
     assert L.fp_plan(P, P, 4, 1, 2048, 128, 128, -0.1, P, ws_bytes, P, P, s) == 3
     assert L.fp_plan(P, P, 4, 1, 2048, 128, 128, float("nan"), P, ws_bytes, P, P, s) == 3
@@ -96,3 +97,47 @@ def test_select_ex_option_validation(lib):
         assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 0, ctypes.byref(opt), P, ws_bytes, P, P,
                                 None, s) == 6
         assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 0, None, P, ws_bytes, P, P, None, s) == 6
+
+
+def test_ragged_sizes(lib):
+    # ragged n (A26): nb = ceil(n / 128); capacity and workspace grow accordingly
+    assert fp.fp_col_idx_capacity(2085) == 17 * 18 // 2
+    assert fp.fp_col_idx_capacity(129) == 3
+    assert fp.fp_workspace_bytes(4, 1, 2085) > fp.fp_workspace_bytes(4, 1, 2048)
+    assert fp.fp_workspace_bytes(4, 1, 129) > 0
+
+
+def test_layout_helpers_and_validation(lib):
+    n, H, G = 1000, 8, 2
+    a = fp.fp_layout_bhsd(3, H, G, n)
+    assert a.batch == 3
+    assert list(a.q_stride) == [H * n * 128, n * 128, 128] == list(a.o_stride)
+    assert list(a.k_stride) == [G * n * 128, n * 128, 128] == list(a.v_stride)
+    b = fp.fp_layout_bshd(2, H, G, n)
+    assert list(b.q_stride) == [n * H * 128, 128, H * 128]
+    assert list(b.k_stride) == [n * G * 128, 128, G * 128]
+    with pytest.raises(fp.FlexPrefillError):
+        fp.fp_layout_bshd(0, H, G, n)
+    P = 0x10000
+    s = ctypes.c_void_p(0)
+    ws_bytes = fp.fp_workspace_bytes(2 * H, 2 * G, n)
+    L = lib
+    bad = fp.fp_layout_bshd(2, H, G, n)
+    bad.k_stride[2] = 1004  # not a multiple of 8 elements
+    assert L.fp_plan_ex(P, P, H, G, n, 128, 128, ctypes.byref(bad), 0.1, P, ws_bytes, P, P, s) == 4
+    bad = fp.fp_layout_bshd(2, H, G, n)
+    bad.q_stride[1] = 64  # rows / heads closer than 128 elements
+    assert L.fp_plan_ex(P, P, H, G, n, 128, 128, ctypes.byref(bad), 0.1, P, ws_bytes, P, P, s) == 2
+    bad = fp.fp_layout_bshd(2, H, G, n)
+    bad.batch = 0
+    assert L.fp_sparse_attn_ex(P, P, P, P, H, G, n, 128, 128, ctypes.byref(bad), P, P, P, 0, s) == 2
+    ok = fp.fp_layout_bshd(2, H, G, n)
+    # the workspace covers batch * heads flattened heads
+    assert L.fp_plan_ex(P, P, H, G, n, 128, 128, ctypes.byref(ok), 0.1, P,
+                        fp.fp_workspace_bytes(H, G, n), P, P, s) == 5
+    import torch
+    if not torch.cuda.is_available():
+        assert L.fp_plan_ex(P, P, H, G, n, 128, 128, ctypes.byref(ok), 0.1, P, ws_bytes, P, P, s) == 6
+        assert L.fp_plan_ex(P, P, H, G, n, 128, 128, None, 0.1, P, ws_bytes, P, P, s) == 6
+        assert L.fp_dense_causal_attn_ex(P, P, P, P, H, G, n, 128, 128, ctypes.byref(ok), None, 0,
+                                         s) == 6

@@ -38,7 +38,7 @@ def _sample_heads(w, k=4):
 def _run(fp, w, heads_checked):
     q, k, v = gen.make_layer_bits(w)
     res = parity.run_gpu(fp, w, q, k, v)
-    nb = w.seq_len // 128
+    nb = -(-w.seq_len // 128)
     m = -(-w.min_budget // 128) if w.min_budget else 0
     # whole-layer properties (every head)
     for h in range(w.heads):

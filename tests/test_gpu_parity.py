@@ -44,7 +44,7 @@ def _check_plan(w, res, plans):
 
 def _check_select_stagewise(w, res, gamma, min_budget):
     dbg = res["dbg"]
-    nb = w.seq_len // 128
+    nb = -(-w.seq_len // 128)
     for h in range(w.heads):
         pat = res["pattern"][h]
         cnt = dbg["sel_count"][h]
@@ -74,7 +74,7 @@ def _check_select_stagewise(w, res, gamma, min_budget):
 
 
 def _check_attn_stagewise(w, res, Q, K, V, qblocks=None):
-    nb = w.seq_len // 128
+    nb = -(-w.seq_len // 128)
     worst_max, worst_mean = 0.0, 0.0
     for h in range(w.heads):
         g = h * w.kv_heads // w.heads
@@ -89,20 +89,27 @@ def _check_attn_stagewise(w, res, Q, K, V, qblocks=None):
 
 
 def test_c1_full_parity(fp):
-    w = C1
+    res = full_parity(fp, C1)
+    # both patterns trigger on the planted workload
+    assert set(res["pattern"].tolist()) == {0, 1}
+
+
+def full_parity(fp, w):
+    """plan, stage-wise selection and attention, end-to-end sets (borderline
+    rule) and outputs, and the dense kernel, all heads."""
     q, k, v = gen.make_layer_bits(w)
     Q, K, V = parity.oracle_inputs(q, k, v)
     res = parity.run_gpu(fp, w, q, k, v, dense=True)
     plans = _oracle_plans(w, Q, K)
     _check_plan(w, res, plans)
-    # both patterns trigger on the planted workload
-    assert set(res["pattern"].tolist()) == {0, 1}
     _check_select_stagewise(w, res, w.gamma, w.min_budget)
     _check_attn_stagewise(w, res, Q, K, V)
     # end-to-end: oracle from scratch, borderline rule
-    nb = w.seq_len // 128
+    nb = -(-w.seq_len // 128)
     for h in range(w.heads):
-        o = oracle.flexprefill_head(Q[h], K[0], V[0], 128, w.gamma, w.tau, 0, with_output=False)
+        g = h * w.kv_heads // w.heads
+        o = oracle.flexprefill_head(Q[h], K[g], V[g], 128, w.gamma, w.tau, w.min_budget,
+                                    with_output=False)
         cnt = res["dbg"]["sel_count"][h]
         if o["pattern"] == oracle.VS:
             for seg, key in ((0, "a_v"), (1, "a_s")):
@@ -116,23 +123,25 @@ def test_c1_full_parity(fp):
         # rows whose block lists match: outputs vs oracle output on the oracle's set
         Mg = parity.csr_mask(res["row_ptr"][h], res["col_idx"][h], nb)
         same = np.all(Mg == o["mask"], axis=1)
-        ref = oracle.sparse_attention(Q[h], K[0], V[0], o["mask"], 128, np.nonzero(same)[0])
+        ref = oracle.sparse_attention(Q[h], K[g], V[g], o["mask"], 128, np.nonzero(same)[0])
         rows = ~np.isnan(ref[:, 0])
         if rows.any():
             d = np.abs(res["out"][h][rows] - ref[rows])
             assert d.max() <= MAX_ABS and d.mean() <= MEAN_ABS
     # dense kernel vs oracle dense causal attention
     for h in range(w.heads):
-        ref = oracle.dense_causal_attention(Q[h], K[0], V[0])
+        g = h * w.kv_heads // w.heads
+        ref = oracle.dense_causal_attention(Q[h], K[g], V[g])
         d = np.abs(res["dense"][h] - ref)
         assert d.max() <= MAX_ABS and d.mean() <= MEAN_ABS, (h, d.max(), d.mean())
+    return res
 
 
 def test_gamma_one_equals_dense(fp):
     w = C1.with_(gamma=1.0)
     q, k, v = gen.make_layer_bits(w)
     res = parity.run_gpu(fp, w, q, k, v, gamma=1.0, dense=True)
-    nb = w.seq_len // 128
+    nb = -(-w.seq_len // 128)
     for h in range(w.heads):
         assert res["row_ptr"][h][-1] == nb * (nb + 1) // 2
     # same kernel, same block order -> bitwise identical to the dense kernel
@@ -275,7 +284,7 @@ def test_selection_variants_stagewise(fp, vs_mode, qa_mode, min_budget, max_budg
     Q, K, V = parity.oracle_inputs(q, k, v)
     res = parity.run_gpu(fp, w, q, k, v, vs_mode=vs_mode, qa_mode=qa_mode, max_budget=max_budget)
     dbg = res["dbg"]
-    nb = w.seq_len // 128
+    nb = -(-w.seq_len // 128)
     assert set(res["pattern"].tolist()) == {0, 1}
     for h in range(w.heads):
         pat = res["pattern"][h]
