@@ -25,14 +25,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-bool make_tile_map(CUtensorMap* map, const void* base, const TLayout& t, int n, int batch) {
+bool make_tile_map(CUtensorMap* map, const void* base, const TLayout& t, int n, int batch,
+                   int box_rows) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[4] = {128, (cuuint64_t)n, (cuuint64_t)t.per, (cuuint64_t)batch};
   // batch stride is unused when batch == 1 but must still be a valid value
   const long long bs = batch > 1 ? t.bs : t.hs * t.per;
   cuuint64_t strides[3] = {(cuuint64_t)t.rs * 2, (cuuint64_t)t.hs * 2, (cuuint64_t)bs * 2};
-  cuuint32_t box[4] = {64, 128, 1, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -211,8 +212,8 @@ static fp_status attn_common(const void* q, const void* k, const void* v, void* 
   const WsLayout L = ws_layout(s);
   CUtensorMap qm, km, vm;
   if (!make_tile_map(&qm, q, lay.q, seq_len, lay.batch) ||
-      !make_tile_map(&km, k, lay.k, seq_len, lay.batch) ||
-      !make_tile_map(&vm, v, lay.v, seq_len, lay.batch))
+      !make_tile_map(&km, k, lay.k, seq_len, lay.batch, attn_kv_box_rows()) ||
+      !make_tile_map(&vm, v, lay.v, seq_len, lay.batch, attn_kv_box_rows()))
     return cuda_status(cudaErrorInvalidValue);
   return cuda_status(launch_attn(s, L, ws, lay, qm, km, vm, o, row_ptr, col_idx, dense,
                                  static_cast<cudaStream_t>(stream)));

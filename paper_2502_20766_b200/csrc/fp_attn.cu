@@ -115,15 +115,30 @@ FP_DEV void exp2_emu2(float x0, float x1, float& y0, float& y1) {
   y1 = __uint_as_float(__float_as_uint(t1) * 8388608u + __float_as_uint(p1));
 }
 
-// D[tmem] (+)= A[tmem] * B[smem]   (A = P, 128 rows x 16 keys, bf16 pairs per column)
-FP_DEV void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                         uint32_t accumulate) {
+// 8 k-steps of one M=128 x N=128 MMA chain in one asm statement: A from TMEM
+// columns a0 + 8 kk, B descriptors b0 + off(kk) (off in 16-B units, added to
+// the start-address field), so the issuing thread does no descriptor math per
+// k-step. acc0: accumulate flag of the first k-step.
+template <uint32_t O1, uint32_t O2, uint32_t O3, uint32_t O4, uint32_t O5, uint32_t O6, uint32_t O7>
+FP_DEV void umma_ts_chain8(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %18, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %9, %17, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %10, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %11, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %12, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %13, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %14, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %15, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %16, %17, p;\n\t}" ::"r"(d),
+      "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "r"(a0 + 32), "r"(a0 + 40), "r"(a0 + 48),
+      "r"(a0 + 56), "l"(b0), "l"(b0 + O1), "l"(b0 + O2), "l"(b0 + O3), "l"(b0 + O4), "l"(b0 + O5),
+      "l"(b0 + O6), "l"(b0 + O7), "r"(idesc), "r"(acc0));
 }
+// k-step offsets (16-B units): K-major SW128 tile of two 16 KiB boxes
+// (kk/4 box, (kk%4)*32 B) and the MN-major V tile (+2048 B per step)
+#define FP_KMAJ_OFFS 2, 4, 6, 1024, 1026, 1028, 1030
+#define FP_MNMAJ_OFFS 128, 256, 384, 512, 640, 768, 896
 
 // One key tile of one softmax warpgroup: S row (128 fp32) from TMEM -> lazy
 // running max -> P = 2^(s - m) (bf16) written over the S columns. Returns the
@@ -308,14 +323,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #endif
         tc_fence_after();
         const uint32_t ka = smem_u32(sm.k[s]);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
 #if FP_QTMEM
-          umma_bf16_ts(tbase + b * 128, tbase + kColQ + kk * 8, sdesc_kmajor(ka, kk), idesc_s, kk > 0);
+        umma_ts_chain8<FP_KMAJ_OFFS>(tbase + b * 128, tbase + kColQ, sdesc_kmajor(ka, 0), idesc_s, 0);
 #else
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
           umma_bf16_ss(tbase + b * 128, sdesc_kmajor(qa, kk), sdesc_kmajor(ka, kk), idesc_s, kk > 0);
 #endif
-        }
         umma_commit(&sm.s_full[b]);
         if (i + kKV < nk) umma_commit(&sm.k_empty[s]);  // the producer waits only for these
       };
@@ -335,10 +349,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         mbar_wait(&sm.p_full[b], (i / kSBuf) & 1);
         tc_fence_after();
         const uint32_t va = smem_u32(sm.v[s]);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16_ts(tbase + kColO, tbase + b * 128 + kk * 8, sdesc_mnmajor(va, kk), idesc_o,
-                       (i > 0 || kk > 0));
+        umma_ts_chain8<FP_MNMAJ_OFFS>(tbase + kColO, tbase + b * 128, sdesc_mnmajor(va, 0), idesc_o,
+                                      i > 0);
         umma_commit(&sm.pv_done[b]);
         if (i + kKV < nk) umma_commit(&sm.v_empty[s]);
         if (i + 2 < nk) issue_s(i + 2);
@@ -448,12 +460,38 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 
 size_t attn_smem_bytes() { return sizeof(AttnSmem); }
 
+cudaError_t launch_attn_v7(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
+                           const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+                           const int32_t* row_ptr, const int32_t* col_idx, bool dense,
+                           cudaStream_t st);
+
+// FP_ATTN_VERSION selects the kernel: 5 = this file (default), 7 = fp_attn7.cu
+// (two warpgroups on interleaved 64-key streams; measured slower, see there)
+#ifndef FP_ATTN_VERSION
+#define FP_ATTN_VERSION 5
+#endif
+#define FP_ATTN_V5 (FP_ATTN_VERSION == 5)
+int attn_kv_box_rows() { return FP_ATTN_V5 ? 128 : 64; }
+
+static cudaError_t launch_attn_v5(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
+                                  const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+                                  const int32_t* row_ptr, const int32_t* col_idx, bool dense,
+                                  cudaStream_t st);
+
 cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layout& lay,
                         const CUtensorMap& qmap, const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                         const int32_t* row_ptr, const int32_t* col_idx, bool dense,
                         cudaStream_t st) {
   (void)L;
   (void)ws;
+  if (FP_ATTN_V5) return launch_attn_v5(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
+  return launch_attn_v7(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
+}
+
+static cudaError_t launch_attn_v5(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
+                                  const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+                                  const int32_t* row_ptr, const int32_t* col_idx, bool dense,
+                                  cudaStream_t st) {
   static bool attr_done = false;
   const size_t smem = attn_smem_bytes();
   if (!attr_done) {

@@ -140,7 +140,10 @@ inline T* wsp(void* ws, size_t off) {
 
 // 4D bf16 tensor map {128 cols, n rows, per heads, batch} with the strides of
 // `t`; box 64 cols x 128 rows, SWIZZLE_128B; rows >= n are zero-filled.
-bool make_tile_map(CUtensorMap* map, const void* base, const TLayout& t, int n, int batch);
+bool make_tile_map(CUtensorMap* map, const void* base, const TLayout& t, int n, int batch,
+                   int box_rows = 128);
+// rows per K/V TMA box of the attention kernel in use (v7: 64-key sub-tiles; v5: 128)
+int attn_kv_box_rows();
 
 // ---- launchers (return cudaGetLastError of their launches) ----
 cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void* q, const void* k,
