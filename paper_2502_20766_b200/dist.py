@@ -57,6 +57,40 @@ def max_heads(H, P):
     return -(-H // P)
 
 
+# ------------------------------------------------ next row f4: balancing ----
+def head_cost(nnz, nb, b=128, d=128):
+    """Useful attention FLOPs of one head with `nnz` computed blocks (the
+    diagonal blocks are half used): 4 d [b^2 (nnz - nb) + nb b (b+1)/2]."""
+    return 4 * d * (b * b * (int(nnz) - nb) + nb * b * (b + 1) // 2)
+
+
+def lpt_assign(costs, P):
+    """Longest-processing-time-first assignment of heads to P ranks: heads in
+    decreasing cost (ties -> lower head index) each go to the currently
+    least-loaded rank (ties -> lower rank). Deterministic, so every rank
+    computes the same assignment from the same (all-gathered) costs.
+    Returns per-rank ascending head lists."""
+    order = sorted(range(len(costs)), key=lambda h: (-costs[h], h))
+    load = [0] * P
+    out = [[] for _ in range(P)]
+    for h in order:
+        r = min(range(P), key=lambda i: (load[i], i))
+        out[r].append(h)
+        load[r] += costs[h]
+    return [sorted(x) for x in out]
+
+
+def imbalance(costs, assignment):
+    """max over ranks of the assigned cost / mean cost (1.0 = perfect)."""
+    loads = [sum(costs[h] for h in hs) for hs in assignment]
+    mean = sum(loads) / len(loads)
+    return max(loads) / mean if mean > 0 else 1.0
+
+
+def static_assignment(H, P):
+    return [list(range(*head_range(H, P, r))) for r in range(P)]
+
+
 def gather_heads(local_out, H, P, group=None):
     """All-gather each rank's [h1-h0][n][d] output slot (padded to ceil(H/P)
     heads) into the full [H][n][d] layer output (torch.distributed)."""
@@ -77,3 +111,102 @@ def gather_heads(local_out, H, P, group=None):
         h0, h1 = head_range(H, P, r)
         idx.extend(range(r * hmax, r * hmax + (h1 - h0)))
     return full[torch.tensor(idx, device=full.device)]
+
+
+class BalancedLayer:
+    """Next row f4: cost-balanced (LPT) attention across ranks, with the output
+    all-gather overlapped with the attention. Every rank holds the whole
+    layer's Q/K/V (replicated inputs) and the full output buffer. One step:
+
+      1. plan + select for this rank's static contiguous head range (the same
+         split as the static partition), written into this rank's CSR slot;
+      2. all-gather of the CSR slots (row_ptr [hmax][nb+1], col_idx
+         [hmax][cap] per rank; NCCL over NVLink);
+      3. per-head costs = useful attention FLOPs from row_ptr[:, nb] (one
+         small device->host read), LPT assignment (deterministic, so every
+         rank computes the same one);
+      4. attention of this rank's LPT heads, one launch per head, each
+         followed by an event on the compute stream;
+      5. broadcast rounds j = 0, 1, ...: every rank broadcasts the output of
+         its j-th head, issued on a communication stream after that head's
+         event, so the exchange overlaps the remaining attention.
+
+    The compute is injected (plan_select(rp_slot, ci_slot), attend(h, rp, ci))
+    so the protocol is testable with the gloo backend on CPU tensors.
+    """
+
+    def __init__(self, H, G, n, world, rank, plan_select, attend, device, group=None, b=128):
+        import torch
+        self.H, self.G, self.n, self.P, self.rank = H, G, n, world, rank
+        self.nb = -(-n // b)
+        self.cap = self.nb * (self.nb + 1) // 2
+        self.hmax = max_heads(H, world)
+        self.ranges = [head_range(H, world, r) for r in range(world)]
+        self.plan_select, self.attend = plan_select, attend
+        self.device, self.group = torch.device(device), group
+        i32 = torch.int32
+        self.rp_slot = torch.zeros((self.hmax, self.nb + 1), dtype=i32, device=device)
+        self.ci_slot = torch.zeros((self.hmax, self.cap), dtype=i32, device=device)
+        self.rp_all = torch.empty((world * self.hmax, self.nb + 1), dtype=i32, device=device)
+        self.ci_all = torch.empty((world * self.hmax, self.cap), dtype=i32, device=device)
+        self.cuda = self.device.type == "cuda"
+        self.comm = torch.cuda.Stream(device=self.device) if self.cuda else None
+        self.last_assignment = None
+        self.last_costs = None
+
+    def slot(self, h):
+        """row of rp_all / ci_all holding head h's CSR."""
+        for r, (h0, h1) in enumerate(self.ranges):
+            if h0 <= h < h1:
+                return r * self.hmax + (h - h0)
+        raise IndexError(h)
+
+    def step(self, out, timers=None):
+        import torch
+        import torch.distributed as dist
+        stream = torch.cuda.current_stream(self.device) if self.cuda else None
+
+        def mark(key):
+            if timers is not None and self.cuda:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                timers.setdefault(key, []).append(ev)
+
+        mark("t0")
+        self.plan_select(self.rp_slot, self.ci_slot)
+        mark("t1")
+        dist.all_gather_into_tensor(self.rp_all, self.rp_slot, group=self.group)
+        dist.all_gather_into_tensor(self.ci_all, self.ci_slot, group=self.group)
+        nnz = self.rp_all[:, self.nb].cpu().tolist()  # the one host read of the step
+        costs = [head_cost(nnz[self.slot(h)], self.nb) for h in range(self.H)]
+        assign = lpt_assign(costs, self.P)
+        self.last_assignment, self.last_costs = assign, costs
+        mark("t2")
+        mine = assign[self.rank]
+        events = []
+        for h in mine:
+            s = self.slot(h)
+            self.attend(h, self.rp_all[s: s + 1], self.ci_all[s: s + 1])
+            if self.cuda:
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                events.append(ev)
+        mark("t3")
+        rounds = max(len(x) for x in assign)
+        if self.cuda:
+            self.comm.wait_stream(stream) if not events else None
+            ctx = torch.cuda.stream(self.comm)
+        else:
+            import contextlib
+            ctx = contextlib.nullcontext()
+        with ctx:
+            for j in range(rounds):
+                if self.cuda and j < len(events):
+                    self.comm.wait_event(events[j])
+                for r in range(self.P):
+                    if j < len(assign[r]):
+                        dist.broadcast(out[assign[r][j]], src=r, group=self.group)
+        if self.cuda:
+            stream.wait_stream(self.comm)
+        mark("t4")
+        return assign
