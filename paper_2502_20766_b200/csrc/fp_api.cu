@@ -301,31 +301,43 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
     char* kd = static_cast<char*>(d_k) + c * kv_bytes;
     char* vd = static_cast<char*>(d_v) + c * kv_bytes;
     char* od = static_cast<char*>(d_o) + c * qb_bytes;
-    cudaEvent_t e_in = nullptr, e_cmp = nullptr;
-    chk(cudaEventCreateWithFlags(&e_in, cudaEventDisableTiming));
-    chk(cudaEventCreateWithFlags(&e_cmp, cudaEventDisableTiming));
+    // K and Q first (all fp_plan / fp_select read), V last (only the attention
+    // reads it); the attention runs one launch per head (bitwise the same
+    // result: work items are per (head, query block)) and each head's output
+    // is copied back as soon as it is done, so only the last head's D2H is
+    // exposed at the end.
+    cudaEvent_t e_kq = nullptr, e_v = nullptr;
+    chk(cudaEventCreateWithFlags(&e_kq, cudaEventDisableTiming));
+    chk(cudaEventCreateWithFlags(&e_v, cudaEventDisableTiming));
     chk(cudaMemcpyAsync(kd, kh, kv_bytes, cudaMemcpyHostToDevice, sin));
     chk(cudaMemcpyAsync(qd, qh, qb_bytes, cudaMemcpyHostToDevice, sin));
+    chk(cudaEventRecord(e_kq, sin));
     chk(cudaMemcpyAsync(vd, vh, kv_bytes, cudaMemcpyHostToDevice, sin));
-    chk(cudaEventRecord(e_in, sin));
-    chk(cudaStreamWaitEvent(scomp, e_in, 0));
-    if (e == cudaSuccess) {
-      void* wsc = static_cast<char*>(ws) + (c % nslots) * slot;
-      int32_t* rp = row_ptr + (size_t)c * g * (nb + 1);
-      int32_t* ci = col_idx + (size_t)c * g * cap;
-      if (!(st = fp_plan(qd, kd, g, 1, seq_len, head_dim, block_size, tau, wsc, slot, pattern + c * g,
-                         jsd + c * g, scomp)) &&
-          !(st = fp_select(g, 1, seq_len, head_dim, block_size, gamma, min_budget, wsc, slot, rp, ci,
-                           nullptr, scomp)))
-        st = fp_sparse_attn(qd, kd, vd, od, g, 1, seq_len, head_dim, block_size, rp, ci, wsc, slot,
-                            scomp);
+    chk(cudaEventRecord(e_v, sin));
+    chk(cudaStreamWaitEvent(scomp, e_kq, 0));
+    void* wsc = static_cast<char*>(ws) + (c % nslots) * slot;
+    int32_t* rp = row_ptr + (size_t)c * g * (nb + 1);
+    int32_t* ci = col_idx + (size_t)c * g * cap;
+    if (e == cudaSuccess &&
+        !(st = fp_plan(qd, kd, g, 1, seq_len, head_dim, block_size, tau, wsc, slot, pattern + c * g,
+                       jsd + c * g, scomp)))
+      st = fp_select(g, 1, seq_len, head_dim, block_size, gamma, min_budget, wsc, slot, rp, ci,
+                     nullptr, scomp);
+    chk(cudaStreamWaitEvent(scomp, e_v, 0));
+    const size_t hb = qb_bytes / g;  // one head of Q / O
+    for (int i = 0; i < g && e == cudaSuccess && st == FP_OK; ++i) {
+      st = fp_sparse_attn(qd + i * hb, kd, vd, od + i * hb, 1, 1, seq_len, head_dim, block_size,
+                          rp + (size_t)i * (nb + 1), ci + (size_t)i * cap, wsc, slot, scomp);
+      cudaEvent_t e_h = nullptr;
+      chk(cudaEventCreateWithFlags(&e_h, cudaEventDisableTiming));
+      chk(cudaEventRecord(e_h, scomp));
+      chk(cudaStreamWaitEvent(sout, e_h, 0));
+      chk(cudaMemcpyAsync(static_cast<char*>(o_host) + c * qb_bytes + i * hb, od + i * hb, hb,
+                          cudaMemcpyDeviceToHost, sout));
+      if (e_h) cudaEventDestroy(e_h);
     }
-    chk(cudaEventRecord(e_cmp, scomp));
-    chk(cudaStreamWaitEvent(sout, e_cmp, 0));
-    chk(cudaMemcpyAsync(static_cast<char*>(o_host) + c * qb_bytes, od, qb_bytes,
-                        cudaMemcpyDeviceToHost, sout));
-    if (e_in) cudaEventDestroy(e_in);
-    if (e_cmp) cudaEventDestroy(e_cmp);
+    if (e_kq) cudaEventDestroy(e_kq);
+    if (e_v) cudaEventDestroy(e_v);
   }
   // join everything back into the caller's stream
   if (e == cudaSuccess) {
