@@ -465,13 +465,19 @@ cudaError_t launch_attn_v7(const Shape& s, const Layout& lay, const CUtensorMap&
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
                            cudaStream_t st);
 
+cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
+                           const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+                           const int32_t* row_ptr, const int32_t* col_idx, bool dense,
+                           cudaStream_t st);
+
 // FP_ATTN_VERSION selects the kernel: 5 = this file (default), 7 = fp_attn7.cu
-// (two warpgroups on interleaved 64-key streams; measured slower, see there)
+// (two warpgroups on interleaved 64-key streams; measured slower, see there),
+// 8 = fp_attn8.cu (q-block pairs sharing K/V loads, ping-pong softmax)
 #ifndef FP_ATTN_VERSION
-#define FP_ATTN_VERSION 5
+#define FP_ATTN_VERSION 8
 #endif
 #define FP_ATTN_V5 (FP_ATTN_VERSION == 5)
-int attn_kv_box_rows() { return FP_ATTN_V5 ? 128 : 64; }
+int attn_kv_box_rows() { return FP_ATTN_VERSION == 7 ? 64 : 128; }
 
 static cudaError_t launch_attn_v5(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                                   const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
@@ -485,6 +491,8 @@ cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layou
   (void)L;
   (void)ws;
   if (FP_ATTN_V5) return launch_attn_v5(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
+  if (FP_ATTN_VERSION == 8)
+    return launch_attn_v8(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
   return launch_attn_v7(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
 }
 

@@ -1,0 +1,473 @@
+// fp_attn8.cu -- stage (iii) of FlexPrefill, y = A(Q, K, V, S) (P:66-83,
+// P:287-288), version 8: two query blocks of one head per CTA sharing their
+// K/V loads, with two ping-ponging softmax warpgroups.
+//
+// Why: v5 (fp_attn.cu) fetches 64 KiB of K/V from L2 for every computed
+// (q-block, k-block) tile. At C3 that is ~290 GB per launch, ~5.4 KB/cycle
+// chip-wide, close to the measured L2 (LTS) throughput cap (~6.3 KB/cycle,
+// B300_MICROARCH.md); ncu: 1820 cycles per tile per SM against 1024 of tensor
+// work. Adjacent query blocks of a head select mostly the same key blocks
+// (shared vertical columns; slash diagonals shifted by one), so a CTA that
+// runs rows qb and qb-1 together loads each key block of the UNION of their
+// lists once: tools/pair_study.py measured 0.58-0.60 union entries per
+// computed tile on C3/C4/C5 (vs 1.0 in v5). The two rows' softmaxes are
+// independent, so two warpgroups work on them out of phase (one
+// exponentiates while the other loads S / stores P / rescales), the
+// FlashAttention-4 ping-pong.
+//
+// One CTA per (head, q-block pair (qbA, qbB = qbA - 1)) work item, 384 threads:
+//   warp 8   K producer   Q_A, Q_B tiles, then the K tiles of the union list
+//                         (merge of the two sorted CSR rows) into a 2-stage ring
+//   warp 10  V producer   the V tiles of the union list into a 3-stage ring
+//   warp 9   MMA issuer   per union entry e and stream X in (A, B): first the
+//                         pending O_X += P_X V (X's previous entry), then, if X
+//                         selected e, S_X = Q_X K_e^T (both operands in smem,
+//                         "SS"). Issue order per shared entry: PV_A S_A PV_B S_B,
+//                         so the tensor core works for one stream while the
+//                         other's softmax runs. A pending PV is issued no later
+//                         than the next union entry (keeps the V ring moving:
+//                         no deadlock when one row skips a run of entries).
+//   warps 0-3 softmax A   one query row per thread (TMEM lane = row, 32x32b
+//   warps 4-7 softmax B   shape, row max/sum thread-local); lazy running max as
+//                         v5 (O rescaled in TMEM only when the max grows by
+//                         > 2^8); P (bf16) over S; final O / l -> global.
+// TMEM (512 columns): S/P_A [0,128) S/P_B [128,256) O_A [256,384) O_B [384,512).
+// S_X of the next entry overwrites P_X right after PV_X is issued: one
+// thread's tcgen05.mma stream executes in order (as in v5).
+// Each row's diagonal block is the last of its own list and takes the
+// intra-block causal mask. When nb is odd the last pair has no row B.
+#include <math.h>
+
+#include "fp_common.cuh"
+#include "fp_internal.h"
+
+namespace fp {
+
+namespace {
+
+constexpr int kThreads8 = 384;
+constexpr int kKS8 = 2, kVS8 = 3;  // K / V ring depths (tiles)
+constexpr uint32_t kColS8 = 0, kColO8 = 256;
+constexpr float kRescale8 = 8.0f;  // lazy rescale: tolerate P up to 2^8 (as v5)
+// exponentials per row and tile (of 128) computed on the FMA pipe instead of
+// the MUFU (16 ex2/clk/SM, the softmax floor: 1024 cycles per 128x128 tile).
+// Measured on B200 (tools/attn_ab2.py block timing, C3 gamma 0.95): 0 -> 34.3
+// ms, 16 -> 34.5, 32 -> 35.5 (dense: 115.4 -> 120.9 at 32): under the 1 kW
+// power cap the extra FMA-pipe work lowers the clock more than it saves.
+#ifndef FP_EMU8
+#define FP_EMU8 0
+#endif
+constexpr int kEmu8 = FP_EMU8;
+
+struct Attn8Smem {
+  uint8_t q[2][kTileBytes];  // Q_A, Q_B (1024-B aligned: first member)
+  uint8_t k[kKS8][kTileBytes];
+  uint8_t v[kVS8][kTileBytes];
+  uint64_t q_full;
+  uint64_t k_full[kKS8], k_empty[kKS8];
+  uint64_t v_full[kVS8], v_empty[kVS8];
+  uint64_t s_full[2], p_full[2], pv_done[2];
+  uint32_t tmem_base;
+};
+
+FP_DEV float fmax3_8(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+FP_DEV void ffma2_8(float& d0, float& d1, float a0, float a1, float b, float c) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\tmov.b64 rc, {%5, %5};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b), "f"(c));
+}
+FP_DEV void fadd2_8(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+FP_DEV void ffma2v_8(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+// 2^x for a pair on the FMA/ALU pipes (FlashAttention-4's MUFU offload):
+// x = j + f (j = rint(x), |f| <= 1/2), 2^f by a degree-3 minimax polynomial
+// (max rel. error 7.5e-5; P is rounded to bf16 afterwards, 2^-9), 2^j added
+// into the exponent field. x is clamped at -125 (masked keys are zeroed
+// separately on the diagonal block).
+FP_DEV void exp2_emu2_8(float x0, float x1, float& y0, float& y1) {
+  const float kMagic = 12582912.0f;  // 1.5 * 2^23: rounds to an integer in the low mantissa bits
+  x0 = fmaxf(x0, -125.0f);
+  x1 = fmaxf(x1, -125.0f);
+  float t0, t1, j0, j1, f0, f1, p0, p1;
+  fadd2_8(t0, t1, x0, x1, kMagic, kMagic);
+  fadd2_8(j0, j1, t0, t1, -kMagic, -kMagic);
+  fadd2_8(f0, f1, x0, x1, -j0, -j1);
+  ffma2_8(p0, p1, f0, f1, 0.0551716626f, 0.242611155f);
+  ffma2v_8(p0, p1, p0, p1, f0, f1, 0.69326099f, 0.69326099f);
+  ffma2v_8(p0, p1, p0, p1, f0, f1, 0.999928072f, 0.999928072f);
+  y0 = __uint_as_float(__float_as_uint(t0) * 8388608u + __float_as_uint(p0));
+  y1 = __uint_as_float(__float_as_uint(t1) * 8388608u + __float_as_uint(p1));
+}
+FP_DEV void tmem_ld_32x32b_x64_8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 " FP_REGLIST64 ", [%64];"
+               : FP_R64(r)
+               : "r"(taddr));
+}
+FP_DEV void tmem_st_32x32b_x64_8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x64.b32 [%64], " FP_REGLIST64 ";"
+               :
+               : FP_W64(r), "r"(taddr));
+}
+
+// S = Q K^T, M=128 N=128, 8 k-steps of 16 in one asm statement, both operands
+// K-major SW128 tiles of two 16 KiB boxes in smem: k-step kk at box kk/4, byte
+// (kk%4)*32 (descriptor start-address offsets in 16-B units: 2, 4, 6, 1024...).
+FP_DEV void umma_ss_chain8(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %9, %17, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %10, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %11, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %12, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %13, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %14, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %15, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %16, %17, p;\n\t}" ::"r"(d),
+      "l"(a0), "l"(a0 + 2), "l"(a0 + 4), "l"(a0 + 6), "l"(a0 + 1024), "l"(a0 + 1026),
+      "l"(a0 + 1028), "l"(a0 + 1030), "l"(b0), "l"(b0 + 2), "l"(b0 + 4), "l"(b0 + 6),
+      "l"(b0 + 1024), "l"(b0 + 1026), "l"(b0 + 1028), "l"(b0 + 1030), "r"(idesc));
+}
+// O += P V, M=128 N=128, 8 k-steps (16 keys each): A = P in TMEM columns
+// a0 + 8 kk, B = V (MN-major SW128) descriptor b0 + kk * 2048 B.
+FP_DEV void umma_pv_chain8(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %18, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %9, %17, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %10, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %11, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %12, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %13, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %14, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %15, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %16, %17, p;\n\t}" ::"r"(d),
+      "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "r"(a0 + 32), "r"(a0 + 40), "r"(a0 + 48),
+      "r"(a0 + 56), "l"(b0), "l"(b0 + 128), "l"(b0 + 256), "l"(b0 + 384), "l"(b0 + 512),
+      "l"(b0 + 640), "l"(b0 + 768), "l"(b0 + 896), "r"(idesc), "r"(acc0));
+}
+
+// Merge of the two rows' sorted key-block lists: next union entry.
+// mask bit 0: row A selected it, bit 1: row B.
+struct UnionIter {
+  const int32_t* la;
+  const int32_t* lb;
+  int na, nb_, ia, ib;
+  bool dense;
+  FP_DEV bool done() const { return ia >= na && ib >= nb_; }
+  FP_DEV int next(int& mask) {
+    const int ka = ia < na ? (dense ? ia : __ldg(la + ia)) : 0x7fffffff;
+    const int kb = ib < nb_ ? (dense ? ib : __ldg(lb + ib)) : 0x7fffffff;
+    const int k = min(ka, kb);
+    mask = (ka == k ? 1 : 0) | (kb == k ? 2 : 0);
+    ia += mask & 1;
+    ib += mask >> 1;
+    return k;
+  }
+};
+
+template <bool DENSE>
+__global__ void __launch_bounds__(kThreads8, 1)
+    attn8_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                 const __grid_constant__ CUtensorMap vmap, __nv_bfloat16* __restrict__ o,
+                 const TLayout ol, int Hp, int Gp, int H, int G, int n, int nb, long long cap,
+                 const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                 float scale_log2) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 tiles need 1024-B alignment
+  Attn8Smem& sm = *reinterpret_cast<Attn8Smem*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int wid = warp_id();
+  // work item (KV-group-major, q-block pairs descending, heads of the group interleaved)
+  const int gsz = H / G;
+  const int npair = (nb + 1) >> 1;
+  const int per_group = gsz * npair;
+  const int g = blockIdx.x / per_group;
+  const int rem = blockIdx.x - g * per_group;
+  const int qbA = nb - 1 - 2 * (rem / gsz);
+  const int qbB = qbA - 1;  // -1: no row B
+  const int h = g * gsz + rem % gsz;
+  int nA, nB;
+  const int32_t* la = nullptr;
+  const int32_t* lb = nullptr;
+  if (DENSE) {
+    nA = qbA + 1;
+    nB = qbB + 1;
+  } else {
+    const int32_t* rp = row_ptr + (size_t)h * (nb + 1);
+    const int bA = rp[qbA];
+    nA = rp[qbA + 1] - bA;
+    la = col_idx + (size_t)h * cap + bA;
+    if (qbB >= 0) {
+      const int bB = rp[qbB];
+      nB = bA - bB;
+      lb = col_idx + (size_t)h * cap + bB;
+    } else {
+      nB = 0;
+    }
+  }
+
+  if (wid == 9) tmem_alloc(&sm.tmem_base, 512);
+  if (tid == 256) {
+    tma_prefetch_desc(&qmap);
+    tma_prefetch_desc(&kmap);
+    tma_prefetch_desc(&vmap);
+    mbar_init(&sm.q_full, 1);
+    for (int s = 0; s < kKS8; ++s) {
+      mbar_init(&sm.k_full[s], 1);
+      mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < kVS8; ++s) {
+      mbar_init(&sm.v_full[s], 1);
+      mbar_init(&sm.v_empty[s], 2);  // two commits per entry (see the issuer)
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&sm.s_full[x], 1);
+      mbar_init(&sm.p_full[x], 4);  // one arrival per softmax warp of the stream
+      mbar_init(&sm.pv_done[x], 1);
+    }
+    mbar_fence_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm.tmem_base;
+
+  if (wid >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    if (wid == 8 || wid == 10) {
+      // ------------------------------------------------ TMA producers (K: warp 8, V: warp 10)
+      if (lane_id() == 0) {
+        const bool isK = (wid == 8);
+        const uint64_t pol = policy_evict_last();
+        if (isK) {
+          mbar_arrive_expect_tx(&sm.q_full, nB > 0 ? 2 * kTileBytes : kTileBytes);
+          tma_tile(sm.q[0], &qmap, &sm.q_full, qbA * 128, h, Hp);
+          if (nB > 0) tma_tile(sm.q[1], &qmap, &sm.q_full, qbB * 128, h, Hp);
+        }
+        const int depth = isK ? kKS8 : kVS8;
+        uint64_t* full = isK ? sm.k_full : sm.v_full;
+        uint64_t* empty = isK ? sm.k_empty : sm.v_empty;
+        const CUtensorMap* map = isK ? &kmap : &vmap;
+        UnionIter it{la, lb, nA, nB, 0, 0, DENSE};
+        int e = 0;
+        for (; !it.done(); ++e) {
+          int mask;
+          const int kb = it.next(mask);
+          const int s = e % depth;
+          if (e >= depth) mbar_wait(&empty[s], ((e - depth) / depth) & 1);
+          mbar_arrive_expect_tx(&full[s], kTileBytes);
+          tma_tile_hint(isK ? sm.k[s] : sm.v[s], map, &full[s], kb * 128, g, Gp, pol);
+        }
+        // drain: the issuer releases every slot it consumes (it does not know
+        // the union length); consume those releases before the CTA exits
+        for (int d = max(0, e - depth); d < e; ++d) mbar_wait(&empty[d % depth], (d / depth) & 1);
+      }
+    } else if (wid == 9) {
+      // ------------------------------------------------ MMA issuer
+      if (lane_id() == 0) {
+        constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false);
+        constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, true);
+        const uint64_t qdesc[2] = {sdesc_kmajor(smem_u32(sm.q[0]), 0), sdesc_kmajor(smem_u32(sm.q[1]), 0)};
+        int pend[2] = {-1, -1};  // union entry of X's S awaiting its PV
+        int cnt[2] = {0, 0};     // S tiles issued per stream
+        auto issue_pv = [&](int x) {
+          const int e = pend[x];
+          const int vs = e % kVS8;
+          mbar_wait(&sm.v_full[vs], (e / kVS8) & 1);
+          mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
+          tc_fence_after();
+          umma_pv_chain8(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128,
+                         sdesc_mnmajor(smem_u32(sm.v[vs]), 0), idesc_o, cnt[x] > 1);
+          umma_commit(&sm.v_empty[vs]);
+          umma_commit(&sm.pv_done[x]);
+          pend[x] = -1;
+        };
+        mbar_wait(&sm.q_full, 0);
+        UnionIter it{la, lb, nA, nB, 0, 0, DENSE};
+        for (int e = 0; !it.done(); ++e) {
+          int mask;
+          it.next(mask);
+          const int ks = e % kKS8;
+          mbar_wait(&sm.k_full[ks], (e / kKS8) & 1);
+          tc_fence_after();
+          const uint64_t kdesc = sdesc_kmajor(smem_u32(sm.k[ks]), 0);
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            if (pend[x] >= 0) issue_pv(x);
+            if (mask & (1 << x)) {
+              umma_ss_chain8(tbase + kColS8 + x * 128, qdesc[x], kdesc, idesc_s);
+              umma_commit(&sm.s_full[x]);
+              pend[x] = e;
+              ++cnt[x];
+            }
+          }
+          umma_commit(&sm.k_empty[ks]);
+          // an entry only one row uses gets its second V-slot release here
+          // (it arrives early, but the phase also needs the PV's commit)
+          if (mask != 3) umma_commit(&sm.v_empty[e % kVS8]);
+        }
+        if (pend[0] >= 0) issue_pv(0);
+        if (pend[1] >= 0) issue_pv(1);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    // ------------------------------------------------ softmax warpgroups
+    const int x = wid >> 2;                     // 0 = row A, 1 = row B
+    const int nX = x ? nB : nA;
+    const int qb = x ? qbB : qbA;
+    const int r = (wid & 3) * 32 + lane_id();   // query row within the block = TMEM lane
+    const uint32_t lane_off = (uint32_t)((wid & 3) * 32) << 16;
+    const uint32_t tS = tbase + kColS8 + x * 128 + lane_off;
+    const uint32_t tO = tbase + kColO8 + x * 128 + lane_off;
+    float m_used = -INFINITY, l = 0.f;
+    for (int t = 0; t < nX; ++t) {
+      mbar_wait(&sm.s_full[x], t & 1);
+      tc_fence_after();
+      float v[128];
+      tmem_ld_32x32b_x64_8(tS, reinterpret_cast<uint32_t*>(v));
+      tmem_ld_32x32b_x64_8(tS + 64, reinterpret_cast<uint32_t*>(v + 64));
+      tmem_wait_ld();
+      if (t == nX - 1) {  // the diagonal block: keys j <= r only
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c > r) v[c] = -INFINITY;
+      }
+      float m0 = fmax3_8(v[0], v[1], v[2]), m1 = fmax3_8(v[3], v[4], v[5]);
+      float m2 = fmax3_8(v[6], v[7], v[8]), m3 = fmax3_8(v[9], v[10], v[11]);
+#pragma unroll
+      for (int c = 12; c < 124; c += 8) {
+        m0 = fmax3_8(m0, v[c], v[c + 1]);
+        m1 = fmax3_8(m1, v[c + 2], v[c + 3]);
+        m2 = fmax3_8(m2, v[c + 4], v[c + 5]);
+        m3 = fmax3_8(m3, v[c + 6], v[c + 7]);
+      }
+      m0 = fmax3_8(m0, v[124], v[125]);
+      m1 = fmax3_8(m1, v[126], v[127]);
+      const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * scale_log2;
+      float alpha = 1.f;
+      if (mx > m_used + kRescale8) {
+        alpha = exp2f(m_used - mx);  // 0 on the first tile
+        m_used = mx;
+      }
+      const float nm = -m_used;
+#pragma unroll
+      for (int c = 0; c < 128; c += 2) ffma2_8(v[c], v[c + 1], v[c], v[c + 1], scale_log2, nm);
+#pragma unroll
+      for (int c = 0; c < 128 - kEmu8; ++c) v[c] = fast_exp2(v[c]);
+#pragma unroll
+      for (int c = 128 - kEmu8; c < 128; c += 2) exp2_emu2_8(v[c], v[c + 1], v[c], v[c + 1]);
+      if (kEmu8 > 0 && t == nX - 1) {
+#pragma unroll
+        for (int c = 128 - kEmu8; c < 128; ++c)
+          if (c > r) v[c] = 0.f;
+      }
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; c += 4) {
+        fadd2_8(s0, s1, s0, s1, v[c], v[c + 1]);
+        fadd2_8(s2, s3, s2, s3, v[c + 2], v[c + 3]);
+      }
+      l = l * alpha + ((s0 + s1) + (s2 + s3));
+      uint32_t pk[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) pk[c] = pack_bf16x2(v[2 * c], v[2 * c + 1]);
+      // O_X holds sum_{earlier} P V once PV of the previous tile is done
+      if (t > 0) {
+        mbar_wait(&sm.pv_done[x], (t - 1) & 1);
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          tc_fence_after();
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t ov[32];
+            tmem_ld32(tO + q4 * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
+            tmem_st32(tO + q4 * 32, ov);
+          }
+        }
+      }
+      tmem_st_32x32b_x64_8(tS, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&sm.p_full[x]);
+    }
+    if (nX > 0) {
+      // epilogue: O / l -> bf16 -> global (rows past n are not stored)
+      mbar_wait(&sm.pv_done[x], (nX - 1) & 1);
+      tc_fence_after();
+      const float il = 1.0f / l;
+      const int row = qb * 128 + r;
+      uint4* dst = reinterpret_cast<uint4*>(o + toff(ol, h, row));
+#pragma unroll
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t ov[32];
+        tmem_ld32(tO + c0, ov);
+        tmem_wait_ld();
+        if (row < n) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 8) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              w[e] = pack_bf16x2(__uint_as_float(ov[c + 2 * e]) * il, __uint_as_float(ov[c + 2 * e + 1]) * il);
+            dst[(c0 + c) / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (wid == 9) tmem_dealloc(tbase, 512);
+}
+
+}  // namespace
+
+size_t attn8_smem_bytes() { return sizeof(Attn8Smem); }
+
+cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
+                           const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+                           const int32_t* row_ptr, const int32_t* col_idx, bool dense,
+                           cudaStream_t st) {
+  static bool attr_done = false;
+  const size_t smem = attn8_smem_bytes();
+  if (!attr_done) {
+    cudaFuncSetAttribute(attn8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(attn8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_done = true;
+  }
+  const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
+  const dim3 grid(s.H * ((s.nb + 1) / 2));
+  auto* op = reinterpret_cast<__nv_bfloat16*>(o);
+  if (dense)
+    attn8_kernel<true><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
+                                                      lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
+                                                      row_ptr, col_idx, scale_log2);
+  else
+    attn8_kernel<false><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
+                                                       lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
+                                                       row_ptr, col_idx, scale_log2);
+  return cudaGetLastError();
+}
+
+}  // namespace fp

@@ -21,6 +21,8 @@ ap.add_argument("--workload", default="C3-llama8b-128k")
 ap.add_argument("--gamma", type=float, default=None)
 ap.add_argument("--reps", type=int, default=12)
 ap.add_argument("--dense", action="store_true")
+ap.add_argument("--blocks", type=int, default=3)
+ap.add_argument("--block-len", type=int, default=12)
 a = ap.parse_args()
 
 fp.load_library(a.libs[0])
@@ -76,3 +78,32 @@ for r in range(a.reps):
 for p, t in zip(a.libs, times):
     t = np.array(t)
     print(f"{os.path.basename(p):18s} {w.name} g={w.gamma}: median {np.median(t):.3f} ms  min {t.min():.3f}  max {t.max():.3f}")
+
+# alternating BLOCKS of back-to-back launches (the power-cap clock settles
+# within a block, as in bench.py's timed steps), SM clock / board power
+# sampled during each block (nvidia-smi, 100 ms): a power-capped kernel shows
+# the clock down and the power at the cap, a latency-bound one neither.
+from bench import ClockSampler  # noqa: E402
+bt = [[] for _ in libs]
+bclk = [[] for _ in libs]
+bpw = [[] for _ in libs]
+for b in range(a.blocks):
+    for i, L in enumerate(libs):
+        with ClockSampler(torch.cuda.current_device()) as cs:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.block_len):
+                call(L)
+            e1.record()
+            torch.cuda.synchronize()
+        bt[i].append(e0.elapsed_time(e1) / a.block_len)
+        for ln in cs.lines:
+            f = ln.split(",")
+            try:
+                bclk[i].append(float(f[0]))
+                bpw[i].append(float(f[2]))
+            except (ValueError, IndexError):
+                pass
+for p, t, c, pw in zip(a.libs, bt, bclk, bpw):
+    print(f"{os.path.basename(p):18s} blocks: median {np.median(t):.3f} ms/launch  min {min(t):.3f}  "
+          f"sm {np.median(c) if c else None} MHz  power {np.median(pw) if pw else None} W")

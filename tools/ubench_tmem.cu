@@ -1,0 +1,205 @@
+// Microbenchmark: TMEM load/store throughput and the cost of one attention
+// softmax tile (128 query rows x 128 keys, one row per thread) on sm_100a,
+// with no tensor-core work, one CTA per SM (148 CTAs), W warps per CTA.
+//   mode 0: tcgen05.ld 32x32b.x64 twice (128 fp32 columns per row) + wait::ld
+//   mode 1: tcgen05.st 32x32b.x64 (64 packed bf16x2 columns per row) + wait::st
+//   mode 2: the full v8 softmax step: ld 128 cols, row max, x*scale - m (FFMA2),
+//           128 ex2, row sum (FADD2), pack to bf16x2, st 64 cols
+//   mode 3: mode 2 without the TMEM traffic (registers only)
+//   mode 4: mode 2 without ex2 (FFMA2 + pack only)
+// Prints cycles per iteration per warp and the per-SM rates.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/ubench_tmem tools/ubench_tmem.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "../paper_2502_20766_b200/csrc/fp_common.cuh"
+
+using namespace fp;
+
+constexpr int ITER = 512;
+
+FP_DEV void ld64(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 " FP_REGLIST64 ", [%64];" : FP_R64(r) : "r"(taddr));
+}
+FP_DEV void st64(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x64.b32 [%64], " FP_REGLIST64 ";" : : FP_W64(r), "r"(taddr));
+}
+FP_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+FP_DEV void ffma2(float& d0, float& d1, float a0, float a1, float b, float c) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\tmov.b64 rc, {%5, %5};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b), "f"(c));
+}
+FP_DEV void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+FP_DEV void exp2_emu2(float x0, float x1, float& y0, float& y1) {
+  const float kMagic = 12582912.0f;
+  x0 = fmaxf(x0, -125.0f);
+  x1 = fmaxf(x1, -125.0f);
+  float t0, t1, j0, j1, f0, f1, p0, p1;
+  fadd2(t0, t1, x0, x1, kMagic, kMagic);
+  fadd2(j0, j1, t0, t1, -kMagic, -kMagic);
+  fadd2(f0, f1, x0, x1, -j0, -j1);
+  ffma2(p0, p1, f0, f1, 0.0551716626f, 0.242611155f);
+  ffma2(p0, p1, p0, p1, f0, 0.69326099f);
+  ffma2(p0, p1, p0, p1, f0, 0.999928072f);
+  y0 = __uint_as_float(__float_as_uint(t0) * 8388608u + __float_as_uint(p0));
+  y1 = __uint_as_float(__float_as_uint(t1) * 8388608u + __float_as_uint(p1));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) kern(int W, long long* out, float* sink) {
+  __shared__ uint32_t tbase_s;
+  if (threadIdx.x < 32) tmem_alloc(&tbase_s, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tbase_s;
+  const int w = threadIdx.x >> 5;
+  if (w < W) {
+    // warp w: lane quarter w & 3, column block (w >> 2) * 128 (two row streams)
+    const uint32_t ta = tb + ((uint32_t)((w & 3) * 32) << 16) + (w >> 2) * 128;
+    float v[128];
+    uint32_t pk[64];
+    float m_used = 0.f, l = 0.f;
+#pragma unroll
+    for (int c = 0; c < 128; ++c) v[c] = (float)(c * 0.01f + threadIdx.x * 1e-3f);
+    const float scale = 0.127f;
+    long long t0 = clock64();
+    for (int it = 0; it < ITER; ++it) {
+      if (MODE == 0 || MODE == 2 || MODE == 4 || MODE >= 5) {
+        ld64(ta, reinterpret_cast<uint32_t*>(v));
+        ld64(ta + 64, reinterpret_cast<uint32_t*>(v + 64));
+        tmem_wait_ld();
+      }
+      if (MODE == 0) {
+        l += v[0] + v[127];
+        continue;
+      }
+      if (MODE == 1) {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) pk[c] = (uint32_t)(it + c);
+        st64(ta, pk);
+        tmem_wait_st();
+        continue;
+      }
+      float m0 = fmax3(v[0], v[1], v[2]), m1 = fmax3(v[3], v[4], v[5]);
+      float m2 = fmax3(v[6], v[7], v[8]), m3 = fmax3(v[9], v[10], v[11]);
+#pragma unroll
+      for (int c = 12; c < 124; c += 8) {
+        m0 = fmax3(m0, v[c], v[c + 1]);
+        m1 = fmax3(m1, v[c + 2], v[c + 3]);
+        m2 = fmax3(m2, v[c + 4], v[c + 5]);
+        m3 = fmax3(m3, v[c + 6], v[c + 7]);
+      }
+      m0 = fmax3(m0, v[124], v[125]);
+      m1 = fmax3(m1, v[126], v[127]);
+      const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * scale;
+      if (mx > m_used + 8.f) m_used = mx;
+      const float nm = -m_used;
+#pragma unroll
+      for (int c = 0; c < 128; c += 2) ffma2(v[c], v[c + 1], v[c], v[c + 1], scale, nm);
+      constexpr int kEmu = MODE == 6 ? 32 : MODE == 7 ? 16 : 0;
+      if (MODE != 4) {
+#pragma unroll
+        for (int c = 0; c < 128 - kEmu; ++c) v[c] = fast_exp2(v[c]);
+#pragma unroll
+        for (int c = 128 - kEmu; c < 128; c += 2) exp2_emu2(v[c], v[c + 1], v[c], v[c + 1]);
+      }
+      if (MODE >= 5) {  // pack + store first, row sum while the store drains
+#pragma unroll
+        for (int c = 0; c < 64; ++c) pk[c] = pack_bf16x2(v[2 * c], v[2 * c + 1]);
+        st64(ta, pk);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; c += 4) {
+          fadd2(s0, s1, s0, s1, v[c], v[c + 1]);
+          fadd2(s2, s3, s2, s3, v[c + 2], v[c + 3]);
+        }
+        l = l * 0.5f + ((s0 + s1) + (s2 + s3));
+        tmem_wait_st();
+        continue;
+      }
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; c += 4) {
+        fadd2(s0, s1, s0, s1, v[c], v[c + 1]);
+        fadd2(s2, s3, s2, s3, v[c + 2], v[c + 3]);
+      }
+      l = l * 0.5f + ((s0 + s1) + (s2 + s3));
+#pragma unroll
+      for (int c = 0; c < 64; ++c) pk[c] = pack_bf16x2(v[2 * c], v[2 * c + 1]);
+      if (MODE == 2 || MODE == 4) {
+        st64(ta, pk);
+        tmem_wait_st();
+      } else {
+#pragma unroll
+        for (int c = 0; c < 128; ++c) v[c] = __uint_as_float(pk[c >> 1] ^ (uint32_t)c);  // keep live
+      }
+    }
+    long long t1 = clock64();
+    if (threadIdx.x % 32 == 0) out[blockIdx.x * 8 + w] = t1 - t0;
+    if (l == 1234.5f) sink[0] = l;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tb, 512);
+}
+
+template <int MODE>
+void run(const char* name, int W, long long* d, float* sink) {
+  kern<MODE><<<148, 256>>>(W, d, sink);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < 20; ++r) kern<MODE><<<148, 256>>>(W, d, sink);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaDeviceSynchronize();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  static long long h[148 * 8];
+  cudaMemcpy(h, d, sizeof(long long) * 148 * 8, cudaMemcpyDeviceToHost);
+  double s = 0;
+  for (int b = 0; b < 148; ++b)
+    for (int w = 0; w < W; ++w) s += h[b * 8 + w];
+  s /= 148.0 * W;
+  const double cyc = s / ITER;  // per iteration per warp (= per 32 rows x 128 cols)
+  // per SM: W warps x 32 rows x 128 cols per iteration
+  const double tiles_per_cyc = W * 32.0 / 128.0 / cyc;
+  const double ns_tile = ms * 1e6 / 20 / (ITER * W * 32.0 / 128.0);
+  printf("%-40s W=%d %8.1f cyc/iter/warp %7.1f cyc/tile/SM %7.1f ns/tile/SM (%.0f MHz) %s\n", name, W, cyc,
+         1.0 / tiles_per_cyc, ns_tile, (1.0 / tiles_per_cyc) / ns_tile * 1e3, cudaGetErrorString(e));
+}
+
+int main() {
+  long long* d;
+  float* sink;
+  cudaMalloc(&d, 148 * 8 * 8);
+  cudaMalloc(&sink, 4);
+  for (int W : {4, 8}) {
+    run<0>("tmem ld 128 cols (64 KiB/tile)", W, d, sink);
+    run<1>("tmem st 64 cols (32 KiB/tile)", W, d, sink);
+    run<2>("softmax step (ld+max+ffma+ex2+sum+pack+st)", W, d, sink);
+    run<3>("softmax step, registers only", W, d, sink);
+    run<4>("softmax step without ex2", W, d, sink);
+    run<5>("softmax step, st before sum", W, d, sink);
+    run<6>("  + 32/128 exp2 on FMA pipe", W, d, sink);
+    run<7>("  + 16/128 exp2 on FMA pipe", W, d, sink);
+  }
+  return 0;
+}
