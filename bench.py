@@ -354,7 +354,7 @@ def run_balanced(a, w, world, rank, local_rank):
             "dense_ms_per_layer": dense_ms,
             "speedup_vs_dense": (dense_ms / ms_step) if dense_ms else None,
             "imbalance": {"lpt": fpdist.imbalance(costs, assign), "static": static_imb},
-            "roofline": {"bound": "tensor", "kernel": "fp_sparse_attn (attn_kernel)",
+            "roofline": {"bound": "tensor", "kernel": "fp_sparse_attn (attn8_kernel)",
                          "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
                          "frac": achieved / peak_sus, "traffic": None,
                          "note": "rank 0's assigned heads over rank 0's attention time"},
@@ -585,7 +585,7 @@ def main():
             "dense_tflops": (dense_flops(H, n) / (dense_ms / 1e3) / 1e12) if dense_ms else None,
             "density": density,
             "patterns": {"qa": int(np.sum(patterns)), "vs": int(len(patterns) - np.sum(patterns))},
-            "roofline": {"bound": "tensor", "kernel": "fp_sparse_attn (attn_kernel)",
+            "roofline": {"bound": "tensor", "kernel": "fp_sparse_attn (attn8_kernel)",
                          "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
                          "frac": achieved / peak_sus, "frac_of_burst": achieved / peak_burst,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)",

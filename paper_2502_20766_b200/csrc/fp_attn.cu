@@ -469,10 +469,15 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
                            cudaStream_t st);
+cudaError_t launch_attn_v9(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
+                           const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+                           const int32_t* row_ptr, const int32_t* col_idx, bool dense,
+                           cudaStream_t st);
 
 // FP_ATTN_VERSION selects the kernel: 5 = this file (default), 7 = fp_attn7.cu
 // (two warpgroups on interleaved 64-key streams; measured slower, see there),
-// 8 = fp_attn8.cu (q-block pairs sharing K/V loads, ping-pong softmax)
+// 8 = fp_attn8.cu (q-block pairs sharing K/V loads, ping-pong softmax),
+// 9 = fp_attn9.cu (q-block pairs sharing K/V loads, v5's single-stream softmax)
 #ifndef FP_ATTN_VERSION
 #define FP_ATTN_VERSION 8
 #endif
@@ -493,6 +498,8 @@ cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layou
   if (FP_ATTN_V5) return launch_attn_v5(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
   if (FP_ATTN_VERSION == 8)
     return launch_attn_v8(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
+  if (FP_ATTN_VERSION == 9)
+    return launch_attn_v9(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
   return launch_attn_v7(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
 }
 

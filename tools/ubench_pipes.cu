@@ -25,6 +25,17 @@ __device__ __forceinline__ uint32_t pack_int(float a, float b) {
   return __byte_perm(ua, ub, 0x7632);
 }
 
+__device__ __forceinline__ uint32_t ex2h2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t ex2bf2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 template <int MODE>
 __global__ void kern(float* out, long long* cyc) {
   float x[8];
@@ -48,6 +59,8 @@ __global__ void kern(float* out, long long* cyc) {
         x[i] = ex2(x[i]) * -0.5f;
         if (i & 1) acc ^= pack_int(x[i - 1], x[i]);
       }
+      if (MODE == 5) x[i] = __uint_as_float(ex2h2(__float_as_uint(x[i])) ^ 0x80008000u);
+      if (MODE == 6) x[i] = __uint_as_float(ex2bf2(__float_as_uint(x[i])) ^ 0x80008000u);
       if (MODE == 4) {
         acc ^= pack_int(x[i], x[(i + 1) & 7]);
         x[i] = __uint_as_float(__float_as_uint(x[i]) ^ (acc & 1u));
@@ -90,5 +103,7 @@ int main() {
   run<4>("integer RNE pack", 8);
   run<2>("2 ex2 + 1 cvt pack (per pair)", 8);
   run<3>("2 ex2 + 1 int pack (per pair)", 8);
+  run<5>("ex2.approx.f16x2 (2 results)", 8);
+  run<6>("ex2.approx.ftz.bf16x2 (2 results)", 8);
   return 0;
 }

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256, 1) kern(int W, long long* out, float* sin
     const float scale = 0.127f;
     long long t0 = clock64();
     for (int it = 0; it < ITER; ++it) {
-      if (MODE == 0 || MODE == 2 || MODE == 4 || MODE >= 5) {
+      if (MODE == 0 || MODE == 2 || MODE == 4 || MODE >= 5) {  // TMEM ld
         ld64(ta, reinterpret_cast<uint32_t*>(v));
         ld64(ta + 64, reinterpret_cast<uint32_t*>(v + 64));
         tmem_wait_ld();
@@ -113,6 +113,31 @@ __global__ void __launch_bounds__(256, 1) kern(int W, long long* out, float* sin
       const float nm = -m_used;
 #pragma unroll
       for (int c = 0; c < 128; c += 2) ffma2(v[c], v[c + 1], v[c], v[c + 1], scale, nm);
+      if (MODE == 8 || MODE == 9) {  // exp on packed half pairs: f16x2 (8) / bf16x2 (9)
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          uint32_t h, e;
+          if (MODE == 8) {
+            asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(h) : "f"(v[2 * c]), "f"(v[2 * c + 1]));
+            asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+            float f0, f1;
+            asm("{.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;}"
+                : "=f"(f0), "=f"(f1) : "r"(e));
+            pk[c] = pack_bf16x2(f0, f1);
+            fadd2(s0, s1, s0, s1, f0, f1);
+          } else {
+            h = pack_bf16x2(v[2 * c], v[2 * c + 1]);
+            asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(e) : "r"(h));
+            pk[c] = e;
+            fadd2(s0, s1, s0, s1, __uint_as_float(e << 16), __uint_as_float(e & 0xffff0000u));
+          }
+        }
+        l = l * 0.5f + (s0 + s1);
+        st64(ta, pk);
+        tmem_wait_st();
+        continue;
+      }
       constexpr int kEmu = MODE == 6 ? 32 : MODE == 7 ? 16 : 0;
       if (MODE != 4) {
 #pragma unroll
@@ -200,6 +225,8 @@ int main() {
     run<5>("softmax step, st before sum", W, d, sink);
     run<6>("  + 32/128 exp2 on FMA pipe", W, d, sink);
     run<7>("  + 16/128 exp2 on FMA pipe", W, d, sink);
+    run<8>("softmax step, ex2.f16x2 (+cvt)", W, d, sink);
+    run<9>("softmax step, ex2.bf16x2", W, d, sink);
   }
   return 0;
 }
