@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1 with --balance lpt: output exchange by NCCL broadcast rounds, or "
+                         "fused into the attention epilogue (peer stores into symmetric memory)")
     ap.add_argument("--balance", default="lpt", choices=["lpt", "static"],
                     help="N > 1: LPT head assignment from the selected CSR (f4) or the static "
                          "contiguous head partition")
@@ -245,7 +248,18 @@ def run_balanced(a, w, world, rank, local_rank):
     k = torch.from_numpy(kb_).view(torch.bfloat16).to(dev)
     v = torch.from_numpy(vb_).view(torch.bfloat16).to(dev)
     del qb_, kb_, vb_
-    out = torch.zeros((H, n, 128), dtype=torch.bfloat16, device=dev)
+    exch = dict(exchange="nccl")
+    if a.exchange == "p2p":
+        # next row f4, fused exchange: the layer output is one symmetric-memory
+        # allocation; every attention launch also stores its rows into the other
+        # ranks' copies over NVLink (fp_sparse_attn_peers), one barrier per step
+        import torch.distributed._symmetric_memory as symm_mem
+        out = symm_mem.empty((H, n, 128), dtype=torch.bfloat16, device=dev)
+        hdl = symm_mem.rendezvous(out, dist.group.WORLD.group_name)
+        exch = dict(exchange="p2p", peer_bases=list(hdl.buffer_ptrs), head_bytes=n * 128 * 2,
+                    barrier=lambda: hdl.barrier(channel=0))
+    else:
+        out = torch.zeros((H, n, 128), dtype=torch.bfloat16, device=dev)
     h0, h1, segs = fpdist.partition(H, G, world)[rank]
     fpls = [(s_, fp.FlexPrefill(s_.h1 - s_.h0, s_.g1 - s_.g0, n, device=dev)) for s_ in segs]
     ws_fpl = fpls[0][1]
@@ -257,12 +271,17 @@ def run_balanced(a, w, world, rank, local_rank):
             rp_slot[s_.h0 - h0: s_.h1 - h0].copy_(f.row_ptr)
             ci_slot[s_.h0 - h0: s_.h1 - h0].copy_(f.col_idx)
 
-    def attend(h, rp, ci):
+    def attend(h, rp, ci, peers=None):
         gg = h // g
-        fp.fp_sparse_attn(q[h: h + 1], k[gg: gg + 1], v[gg: gg + 1], out[h: h + 1], 1, 1, n, rp, ci,
-                          ws_fpl.ws, ws_fpl.ws_bytes)
+        if peers is None:
+            fp.fp_sparse_attn(q[h: h + 1], k[gg: gg + 1], v[gg: gg + 1], out[h: h + 1], 1, 1, n, rp,
+                              ci, ws_fpl.ws, ws_fpl.ws_bytes)
+        else:
+            fp.fp_sparse_attn_peers(q[h: h + 1], k[gg: gg + 1], v[gg: gg + 1], out[h: h + 1], peers,
+                                    peers.numel(), 1, 1, n, rp, ci, ws=ws_fpl.ws,
+                                    ws_bytes=ws_fpl.ws_bytes)
 
-    layer = fpdist.BalancedLayer(H, G, n, world, rank, plan_select, attend, dev)
+    layer = fpdist.BalancedLayer(H, G, n, world, rank, plan_select, attend, dev, **exch)
     stream = torch.cuda.current_stream()
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
@@ -348,7 +367,9 @@ def run_balanced(a, w, world, rank, local_rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded planted sink/vertical/slash/diverse structure, synth/gen.py)",
             "config": dict(w.describe(), parallelism=f"LPT heads over {world} ranks (replicated "
-                           "inputs) + CSR all-gather + overlapped output broadcasts",
+                           "inputs) + CSR all-gather + " + (
+                               "output stores fused into the attention epilogue (symmetric memory)"
+                               if a.exchange == "p2p" else "overlapped output broadcasts"),
                            l2=l2_note(w)),
             "latency_ms_per_layer": ms_step, "stage_ms_rank0": stages,
             "dense_ms_per_layer": dense_ms,

@@ -203,6 +203,31 @@ fp_status fp_sparse_attn_ex(const void* q, const void* k, const void* v, void* o
                             const fp_layout* layout, const int32_t* row_ptr,
                             const int32_t* col_idx, void* ws, size_t ws_bytes, void* stream);
 
+/* Next row f4: fp_sparse_attn_ex whose epilogue also stores
+ * every output row into n_peer further buffers -- the output exchange of the
+ * head-partitioned multi-GPU layer (§8(e)) fused into the attention kernel.
+ * Each peer buffer is another rank's output mapped into this process (CUDA IPC
+ * / torch symmetric memory over NVLink), so a rank's heads reach every rank
+ * tile by tile while its later tiles compute, instead of a separate
+ * all-gather or broadcast after the kernel.
+ *   peer_o   DEVICE array [n_peer] of device pointers (8-B aligned array);
+ *            each buffer has o's layout (plain [heads][seq_len][128], or
+ *            layout->o strides) and receives exactly the rows written to o
+ *   n_peer   0..FP_MAX_PEERS (0: identical to fp_sparse_attn_ex)
+ * Completion on the peers is the caller's: a cross-rank barrier ordered after
+ * the kernel (e.g. the symmetric-memory barrier on the same stream) before a
+ * peer reads its buffer. Errors: FP_ERR_RANGE n_peer < 0 or > FP_MAX_PEERS;
+ * FP_ERR_NULL peer_o NULL with n_peer > 0; FP_ERR_ALIGN peer_o not 8-B
+ * aligned (the pointer values are device data and are not checked). Only the
+ * default attention kernel (v8) implements it; others fail with FP_ERR_CUDA
+ * (cudaErrorNotSupported). */
+#define FP_MAX_PEERS 8
+fp_status fp_sparse_attn_peers(const void* q, const void* k, const void* v, void* o,
+                               const void* const* peer_o, int n_peer, int heads, int kv_heads,
+                               int seq_len, int head_dim, int block_size, const fp_layout* layout,
+                               const int32_t* row_ptr, const int32_t* col_idx, void* ws,
+                               size_t ws_bytes, void* stream);
+
 /* Dense causal attention A(Q, K, V) with the same kernel (every kb <= qb). */
 fp_status fp_dense_causal_attn(const void* q, const void* k, const void* v, void* o, int heads,
                                int kv_heads, int seq_len, int head_dim, int block_size,

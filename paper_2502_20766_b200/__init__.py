@@ -99,6 +99,8 @@ def load_library(path=LIB_PATH):
                                    _P, _P, _Z, _P]),
         "fp_dense_causal_attn_ex": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, ctypes.POINTER(Layout),
                                          _P, _Z, _P]),
+        "fp_sparse_attn_peers": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I,
+                                      ctypes.POINTER(Layout), _P, _P, _P, _Z, _P]),
         "fp_kernels_per_layer": (_I, []),
         "fp_status_string": (ctypes.c_char_p, [_I]),
         "fp_last_cuda_error": (_I, []),
@@ -225,6 +227,18 @@ def fp_sparse_attn_ex(q, k, v, o, heads, kv_heads, seq_len, layout, row_ptr, col
     _check("fp_sparse_attn_ex", _L().fp_sparse_attn_ex(
         _ptr(q), _ptr(k), _ptr(v), _ptr(o), heads, kv_heads, seq_len, head_dim, block_size,
         _lay(layout), _ptr(row_ptr), _ptr(col_idx), _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def fp_sparse_attn_peers(q, k, v, o, peer_o, n_peer, heads, kv_heads, seq_len, row_ptr, col_idx,
+                         layout=None, ws=None, ws_bytes=0, stream=None, head_dim=128,
+                         block_size=128):
+    """fp_sparse_attn whose epilogue also stores every output row into n_peer
+    further buffers; peer_o: device int64 tensor (or address) of n_peer device
+    pointers (next row f4: the fused output exchange)."""
+    _check("fp_sparse_attn_peers", _L().fp_sparse_attn_peers(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(peer_o), n_peer, heads, kv_heads, seq_len,
+        head_dim, block_size, _lay(layout), _ptr(row_ptr), _ptr(col_idx), _ptr(ws), ws_bytes,
+        _stream(stream)))
 
 
 def fp_dense_causal_attn_ex(q, k, v, o, heads, kv_heads, seq_len, layout, ws=None, ws_bytes=0,

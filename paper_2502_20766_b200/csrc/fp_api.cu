@@ -198,8 +198,11 @@ static fp_status attn_common(const void* q, const void* k, const void* v, void* 
                              int kv_heads, int seq_len, int head_dim, int block_size,
                              const fp_layout* layout, const int32_t* row_ptr,
                              const int32_t* col_idx, void* ws, size_t ws_bytes, void* stream,
-                             bool dense) {
+                             bool dense, const void* const* peer_o = nullptr, int n_peer = 0) {
   if (!q || !k || !v || !o) return FP_ERR_NULL;
+  if (n_peer < 0 || n_peer > FP_MAX_PEERS) return FP_ERR_RANGE;
+  if (n_peer > 0 && !peer_o) return FP_ERR_NULL;
+  if (n_peer > 0 && (reinterpret_cast<uintptr_t>(peer_o) & 7u)) return FP_ERR_ALIGN;
   if (!dense && (!row_ptr || !col_idx)) return FP_ERR_NULL;
   fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
   if (st) return st;
@@ -215,8 +218,8 @@ static fp_status attn_common(const void* q, const void* k, const void* v, void* 
       !make_tile_map(&km, k, lay.k, seq_len, lay.batch, attn_kv_box_rows()) ||
       !make_tile_map(&vm, v, lay.v, seq_len, lay.batch, attn_kv_box_rows()))
     return cuda_status(cudaErrorInvalidValue);
-  return cuda_status(launch_attn(s, L, ws, lay, qm, km, vm, o, row_ptr, col_idx, dense,
-                                 static_cast<cudaStream_t>(stream)));
+  return cuda_status(launch_attn(s, L, ws, lay, qm, km, vm, o, row_ptr, col_idx, dense, peer_o,
+                                 n_peer, static_cast<cudaStream_t>(stream)));
 }
 
 fp_status fp_sparse_attn(const void* q, const void* k, const void* v, void* o, int heads,
@@ -233,6 +236,15 @@ fp_status fp_sparse_attn_ex(const void* q, const void* k, const void* v, void* o
                             const int32_t* col_idx, void* ws, size_t ws_bytes, void* stream) {
   return attn_common(q, k, v, o, heads, kv_heads, seq_len, head_dim, block_size, layout, row_ptr,
                      col_idx, ws, ws_bytes, stream, false);
+}
+
+fp_status fp_sparse_attn_peers(const void* q, const void* k, const void* v, void* o,
+                               const void* const* peer_o, int n_peer, int heads, int kv_heads,
+                               int seq_len, int head_dim, int block_size, const fp_layout* layout,
+                               const int32_t* row_ptr, const int32_t* col_idx, void* ws,
+                               size_t ws_bytes, void* stream) {
+  return attn_common(q, k, v, o, heads, kv_heads, seq_len, head_dim, block_size, layout, row_ptr,
+                     col_idx, ws, ws_bytes, stream, false, peer_o, n_peer);
 }
 
 fp_status fp_dense_causal_attn(const void* q, const void* k, const void* v, void* o, int heads,

@@ -468,7 +468,7 @@ cudaError_t launch_attn_v7(const Shape& s, const Layout& lay, const CUtensorMap&
 cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
-                           cudaStream_t st);
+                           const void* const* peer_o, int n_peer, cudaStream_t st);
 cudaError_t launch_attn_v9(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
@@ -492,12 +492,13 @@ static cudaError_t launch_attn_v5(const Shape& s, const Layout& lay, const CUten
 cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layout& lay,
                         const CUtensorMap& qmap, const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                         const int32_t* row_ptr, const int32_t* col_idx, bool dense,
-                        cudaStream_t st) {
+                        const void* const* peer_o, int n_peer, cudaStream_t st) {
   (void)L;
   (void)ws;
-  if (FP_ATTN_V5) return launch_attn_v5(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
   if (FP_ATTN_VERSION == 8)
-    return launch_attn_v8(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
+    return launch_attn_v8(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, peer_o, n_peer, st);
+  if (n_peer > 0) return cudaErrorNotSupported;  // the fused output exchange is v8's
+  if (FP_ATTN_V5) return launch_attn_v5(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
   if (FP_ATTN_VERSION == 9)
     return launch_attn_v9(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);
   return launch_attn_v7(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, st);

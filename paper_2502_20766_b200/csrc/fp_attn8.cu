@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
                  const __grid_constant__ CUtensorMap vmap, __nv_bfloat16* __restrict__ o,
                  const TLayout ol, int Hp, int Gp, int H, int G, int n, int nb, long long cap,
                  const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                 float scale_log2) {
+                 float scale_log2, const unsigned long long* __restrict__ peer_o, int n_peer) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 tiles need 1024-B alignment
   Attn8Smem& sm = *reinterpret_cast<Attn8Smem*>(smem_raw);
@@ -417,20 +417,30 @@ __global__ void __launch_bounds__(kThreads8, 1)
       tc_fence_after();
       const float il = 1.0f / l;
       const int row = qb * 128 + r;
-      uint4* dst = reinterpret_cast<uint4*>(o + toff(ol, h, row));
+      const size_t off = toff(ol, h, row);
+      uint4* dst = reinterpret_cast<uint4*>(o + off);
 #pragma unroll
       for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t ov[32];
         tmem_ld32(tO + c0, ov);
         tmem_wait_ld();
         if (row < n) {
+          uint4 w4[4];
 #pragma unroll
           for (int c = 0; c < 32; c += 8) {
             uint32_t w[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e)
               w[e] = pack_bf16x2(__uint_as_float(ov[c + 2 * e]) * il, __uint_as_float(ov[c + 2 * e + 1]) * il);
-            dst[(c0 + c) / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+            w4[c / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[(c0 + c) / 8] = w4[c / 8];
+          }
+          // next row f4: the same row into every peer's output buffer (another
+          // rank's buffer mapped into this process: the stores go over NVLink)
+          for (int i = 0; i < n_peer; ++i) {
+            uint4* pd = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(__ldg(peer_o + i)) + off);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) pd[c0 / 8 + c] = w4[c];
           }
         }
       }
@@ -448,7 +458,7 @@ size_t attn8_smem_bytes() { return sizeof(Attn8Smem); }
 cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
-                           cudaStream_t st) {
+                           const void* const* peer_o, int n_peer, cudaStream_t st) {
   static bool attr_done = false;
   const size_t smem = attn8_smem_bytes();
   if (!attr_done) {
@@ -462,11 +472,15 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
   if (dense)
     attn8_kernel<true><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
                                                       lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
-                                                      row_ptr, col_idx, scale_log2);
+                                                      row_ptr, col_idx, scale_log2,
+                                                      reinterpret_cast<const unsigned long long*>(peer_o),
+                                                      n_peer);
   else
     attn8_kernel<false><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
                                                        lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
-                                                       row_ptr, col_idx, scale_log2);
+                                                       row_ptr, col_idx, scale_log2,
+                                                       reinterpret_cast<const unsigned long long*>(peer_o),
+                                                       n_peer);
   return cudaGetLastError();
 }
 

@@ -155,6 +155,6 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
 cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layout& lay,
                         const CUtensorMap& qmap, const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                         const int32_t* row_ptr, const int32_t* col_idx, bool dense,
-                        cudaStream_t st);
+                        const void* const* peer_o, int n_peer, cudaStream_t st);
 
 }  // namespace fp

@@ -131,11 +131,21 @@ class BalancedLayer:
          its j-th head, issued on a communication stream after that head's
          event, so the exchange overlaps the remaining attention.
 
+    exchange="p2p" (next row f4, the fused exchange): instead of step 5, the
+    attention kernel's epilogue stores each output row into every rank's
+    output buffer as well (fp_sparse_attn_peers over NVLink; the buffers are
+    one symmetric-memory allocation whose peer base addresses are
+    `peer_bases`), and one cross-rank barrier (`barrier`, stream-ordered on
+    the GPU) ends the step. attend is then called as attend(h, rp, ci, peers)
+    with `peers` the device table of the other ranks' head-h addresses
+    (peer_table(h)), or None at one rank.
+
     The compute is injected (plan_select(rp_slot, ci_slot), attend(h, rp, ci))
     so the protocol is testable with the gloo backend on CPU tensors.
     """
 
-    def __init__(self, H, G, n, world, rank, plan_select, attend, device, group=None, b=128):
+    def __init__(self, H, G, n, world, rank, plan_select, attend, device, group=None, b=128,
+                 exchange="nccl", peer_bases=None, head_bytes=None, barrier=None):
         import torch
         self.H, self.G, self.n, self.P, self.rank = H, G, n, world, rank
         self.nb = -(-n // b)
@@ -153,6 +163,22 @@ class BalancedLayer:
         self.comm = torch.cuda.Stream(device=self.device) if self.cuda else None
         self.last_assignment = None
         self.last_costs = None
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError(exchange)
+        self.exchange = exchange
+        self.barrier = barrier
+        self.peer_tab = None
+        if exchange == "p2p":
+            if barrier is None or head_bytes is None or peer_bases is None or len(peer_bases) != world:
+                raise ValueError("exchange='p2p' needs peer_bases (one per rank), head_bytes, barrier")
+            others = [r for r in range(world) if r != rank]
+            # row h: the other ranks' addresses of head h (device int64 table)
+            tab = [[int(peer_bases[r]) + h * int(head_bytes) for r in others] for h in range(H)]
+            self.peer_tab = torch.tensor(tab, dtype=torch.int64, device=device) if others else None
+
+    def peer_table(self, h):
+        """device int64 [P-1] of the other ranks' output addresses of head h (p2p), or None"""
+        return None if self.peer_tab is None else self.peer_tab[h]
 
     def slot(self, h):
         """row of rp_all / ci_all holding head h's CSR."""
@@ -183,6 +209,16 @@ class BalancedLayer:
         self.last_assignment, self.last_costs = assign, costs
         mark("t2")
         mine = assign[self.rank]
+        if self.exchange == "p2p":
+            # fused exchange: every launch also stores its rows into the peers'
+            # buffers; one barrier after the last launch completes the layer
+            for h in mine:
+                s = self.slot(h)
+                self.attend(h, self.rp_all[s: s + 1], self.ci_all[s: s + 1], self.peer_table(h))
+            mark("t3")
+            self.barrier()
+            mark("t4")
+            return assign
         events = []
         for h in mine:
             s = self.slot(h)

@@ -141,3 +141,22 @@ def test_layout_helpers_and_validation(lib):
         assert L.fp_plan_ex(P, P, H, G, n, 128, 128, None, 0.1, P, ws_bytes, P, P, s) == 6
         assert L.fp_dense_causal_attn_ex(P, P, P, P, H, G, n, 128, 128, ctypes.byref(ok), None, 0,
                                          s) == 6
+
+
+def test_peers_validation(lib):
+    """fp_sparse_attn_peers (next row f4): argument checks before any device work."""
+    P = 0x10000
+    s = ctypes.c_void_p(0)
+    H, G, n = 4, 1, 2048
+    L = lib
+    f = L.fp_sparse_attn_peers
+    assert f(P, P, P, P, P, 9, H, G, n, 128, 128, None, P, P, P, 0, s) == 3   # n_peer > FP_MAX_PEERS
+    assert f(P, P, P, P, P, -1, H, G, n, 128, 128, None, P, P, P, 0, s) == 3
+    assert f(P, P, P, P, None, 2, H, G, n, 128, 128, None, P, P, P, 0, s) == 1  # peer_o NULL
+    assert f(P, P, P, P, P + 4, 2, H, G, n, 128, 128, None, P, P, P, 0, s) == 4  # peer_o not 8-B aligned
+    assert f(P, P, P, P, P, 2, H, G, n, 128, 128, None, None, P, P, 0, s) == 1  # CSR NULL
+    assert f(P, P, P, P, P, 2, H, 3, n, 128, 128, None, P, P, P, 0, s) == 2
+    import torch
+    if not torch.cuda.is_available():
+        assert f(P, P, P, P, P, 2, H, G, n, 128, 128, None, P, P, P, 0, s) == 6
+        assert f(P, P, P, P, None, 0, H, G, n, 128, 128, None, P, P, P, 0, s) == 6

@@ -105,3 +105,81 @@ def test_balanced_layer_gloo(world, H, G):
     assigns = {tuple(map(tuple, a)) for _, _, a in res}
     assert len(assigns) == 1  # every rank computed the same assignment
     assert all(ok for _, ok, _ in res)  # every rank holds the full, correct output
+
+
+def _worker_p2p(rank, world, port, H, G, n, outs, q):
+    """exchange='p2p': each rank's attend stores its head into EVERY rank's
+    buffer (shared-memory CPU tensors stand in for the NVLink-mapped peer
+    buffers), then one barrier; no broadcast rounds."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        b, d = 4, 3
+        nb = -(-n // b)
+        h0, h1 = D.head_range(H, world, rank)
+        bases = [(r + 1) << 40 for r in range(world)]
+        head_bytes = n * d * 2
+
+        def plan_select(rp_slot, ci_slot):
+            for i, h in enumerate(range(h0, h1)):
+                rows = fake_csr(h, nb)
+                off = 0
+                rp_slot[i, 0] = 0
+                for qb, ks in enumerate(rows):
+                    ci_slot[i, off: off + len(ks)] = torch.tensor(ks, dtype=torch.int32)
+                    off += len(ks)
+                    rp_slot[i, qb + 1] = off
+
+        seen = []
+
+        def attend(h, rp, ci, peers):
+            rows = [ci[0, rp[0, qb]: rp[0, qb + 1]].tolist() for qb in range(nb)]
+            assert rows == fake_csr(h, nb)
+            others = [r for r in range(world) if r != rank]
+            assert peers.tolist() == [bases[r] + h * head_bytes for r in others]
+            val = fake_out(h, rows, n, d)
+            outs[rank][h] = val          # the kernel's own store
+            for r in others:             # the fused peer stores
+                outs[r][h] = val
+            seen.append(h)
+
+        L = D.BalancedLayer(H, G, n, world, rank, plan_select, attend, "cpu", b=b, exchange="p2p",
+                            peer_bases=bases, head_bytes=head_bytes,
+                            barrier=lambda: dist.barrier())
+        assign = L.step(outs[rank])
+        exp = torch.stack([fake_out(h, fake_csr(h, nb), n, d) for h in range(H)])
+        q.put((rank, bool(torch.equal(outs[rank], exp)), assign, sorted(seen)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,H,G", [(2, 8, 2), (3, 7, 7)])
+def test_balanced_layer_p2p_gloo(world, H, G):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n, d = 24, 3
+    outs = [torch.full((H, n, d), -1.0).share_memory_() for _ in range(world)]
+    ps = [ctx.Process(target=_worker_p2p, args=(r, world, port, H, G, n, outs, q))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assigns = {tuple(map(tuple, a)) for _, _, a, _ in res}
+    assert len(assigns) == 1
+    assign = list(assigns)[0]
+    for rank, ok, _, seen in res:
+        assert ok, rank                         # full output on every rank after the barrier
+        assert seen == sorted(assign[rank])     # each rank computed exactly its LPT heads
+
+
+def test_p2p_requires_peer_info():
+    with pytest.raises(ValueError):
+        D.BalancedLayer(4, 1, 16, 2, 0, None, None, "cpu", b=4, exchange="p2p")
+    with pytest.raises(ValueError):
+        D.BalancedLayer(4, 1, 16, 2, 0, None, None, "cpu", b=4, exchange="nvshmem")

@@ -54,6 +54,22 @@ def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flus
         fpl.attn(q, k, v, out)
 
     ms = timed(layer, steps, warmup)
+    # the same layer replayed from one CUDA graph (no host launch gaps: short
+    # sequences are launch-bound when timed eagerly)
+    g = fpl.capture_layer(q, k, v, out, gamma=w.gamma, tau=w.tau, min_budget=w.min_budget) \
+        if not opts else None
+    ms_graph = timed(g.replay, steps, warmup) if g is not None else None
+    gd = None
+    if dense:
+        import torch as _t
+        side = _t.cuda.Stream()
+        side.wait_stream(_t.cuda.current_stream())
+        with _t.cuda.stream(side):
+            fpl.dense(q, k, v, out)
+            gd = _t.cuda.CUDAGraph()
+            with _t.cuda.graph(gd, stream=side):
+                fpl.dense(q, k, v, out)
+        _t.cuda.current_stream().wait_stream(side)
     fpl.plan(q, k, w.tau)
     fpl.select(w.gamma, w.min_budget, **opts)
     torch.cuda.synchronize()
@@ -68,11 +84,14 @@ def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flus
     nnz = [s_["nnz_blocks"] for s_ in stats]
     pats = [s_["pattern"] for s_ in stats]
     dms = timed(lambda: fpl.dense(q, k, v, out), max(2, steps // 2), 1) if dense else None
+    dms_graph = timed(gd.replay, max(2, steps // 2), 1) if gd is not None else None
     return {
         "workload": w.name, "heads": w.heads, "kv_heads": w.kv_heads, "seq_len": w.seq_len,
         "gamma": w.gamma, "tau": w.tau, "min_budget": w.min_budget, "select_options": opts,
         "layer_ms": ms, "tokens_per_s": w.seq_len / (ms / 1e3), "attn_ms": attn_ms,
         "dense_ms": dms, "speedup_vs_dense": (dms / ms) if dms else None,
+        "layer_ms_graph": ms_graph, "dense_ms_graph": dms_graph,
+        "speedup_vs_dense_graph": (dms_graph / ms_graph) if (dms_graph and ms_graph) else None,
         "density": float(np.sum(nnz)) / (len(nnz) * nb * (nb + 1) / 2),
         "qa_heads": int(np.sum(pats)), "vs_heads": int(len(pats) - np.sum(pats)),
         "budget_added": int(sum(s_["budget_added"] for s_ in stats)),
@@ -94,6 +113,10 @@ def points(which):
         for mb in (1024, 0):
             for g in C.C4_GAMMAS:
                 yield C.C4.with_(gamma=g, min_budget=mb), None
+    elif which == "c5short":
+        for base in (C.C5_QWEN, C.C5_YI):
+            for n in (4096, 8192, 16384):
+                yield base.with_(seq_len=n, name=f"{base.name}-{n // 1024}k"), None
     elif which == "c5":
         for base in (C.C5_QWEN, C.C5_YI):
             for n in C.C5_LENGTHS:
