@@ -30,8 +30,10 @@
  *  - Validation is synchronous and happens before anything is enqueued; an
  *    invalid call enqueues nothing and returns a non-zero fp_status:
  *      FP_ERR_NULL      a required pointer is NULL
- *      FP_ERR_SHAPE     heads % kv_heads != 0, seq_len < block_size,
- *                       seq_len > 2^20, head_dim != 128, block_size != 128,
+ *      FP_ERR_SHAPE     heads % kv_heads != 0, seq_len < 128, head_dim != 128,
+ *                       block_size not 64 or 128 (128 is the
+ *                       B200 tile, 64 the paper's alternative, A27), more than
+ *                       8192 blocks (seq_len > 2^20 at b = 128, 2^19 at b = 64),
  *                       an fp_layout with batch < 1 or a stride < 128 elements
  *      FP_ERR_RANGE     gamma <= 0 or NaN; tau outside [0,1] or NaN; min_budget < 0
  *                       (gamma >= 1 is allowed and selects every causal block, A7)
@@ -219,8 +221,8 @@ fp_status fp_sparse_attn_ex(const void* q, const void* k, const void* v, void* o
  * peer reads its buffer. Errors: FP_ERR_RANGE n_peer < 0 or > FP_MAX_PEERS;
  * FP_ERR_NULL peer_o NULL with n_peer > 0; FP_ERR_ALIGN peer_o not 8-B
  * aligned (the pointer values are device data and are not checked). Only the
- * default attention kernel (v8) implements it; others fail with FP_ERR_CUDA
- * (cudaErrorNotSupported). */
+ * default attention kernel (v8) at block_size 128 implements it; otherwise the
+ * call fails with FP_ERR_CUDA (cudaErrorNotSupported). */
 #define FP_MAX_PEERS 8
 fp_status fp_sparse_attn_peers(const void* q, const void* k, const void* v, void* o,
                                const void* const* peer_o, int n_peer, int heads, int kv_heads,

@@ -263,7 +263,8 @@ class FlexPrefill:
     layout of a QKV projection) use the *_ex entry points; per-head buffers
     (pattern, jsd, CSR, stats) then cover batch * heads flattened heads."""
 
-    def __init__(self, heads, kv_heads, seq_len, device="cuda", batch=1, layout="bhsd"):
+    def __init__(self, heads, kv_heads, seq_len, device="cuda", batch=1, layout="bhsd",
+                 block_size=128):
         import torch
         if layout not in ("bhsd", "bshd"):
             raise ValueError(layout)
@@ -274,11 +275,12 @@ class FlexPrefill:
             self.layout = mk(batch, heads, kv_heads, seq_len)
         heads, kv_heads = batch * heads, batch * kv_heads  # flattened
         self.H, self.G, self.n = heads, kv_heads, seq_len
-        self.nb = -(-seq_len // 128)
-        self.ws_bytes = fp_workspace_bytes(heads, kv_heads, seq_len)
+        self.b = block_size
+        self.nb = -(-seq_len // block_size)
+        self.ws_bytes = fp_workspace_bytes(heads, kv_heads, seq_len, block_size=block_size)
         if self.ws_bytes == 0:
             raise FlexPrefillError("fp_workspace_bytes", 2)
-        self.cap = fp_col_idx_capacity(seq_len)
+        self.cap = fp_col_idx_capacity(seq_len, block_size)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
         self.pattern = torch.empty(heads, dtype=torch.int32, device=device)
         self.jsd = torch.empty(heads, dtype=torch.float32, device=device)
@@ -290,31 +292,33 @@ class FlexPrefill:
     def plan(self, q, k, tau=0.1, stream=None):
         if self.layout is not None:
             fp_plan_ex(q, k, self.heads, self.kv_heads, self.n, self.layout, tau, self.ws,
-                       self.ws_bytes, self.pattern, self.jsd, stream)
+                       self.ws_bytes, self.pattern, self.jsd, stream, block_size=self.b)
             return
         fp_plan(q, k, self.H, self.G, self.n, tau, self.ws, self.ws_bytes, self.pattern, self.jsd,
-                stream)
+                stream, block_size=self.b)
 
     def select(self, gamma=0.95, min_budget=0, stream=None, with_stats=True, vs_mode=0, qa_mode=0,
                max_budget=0):
         fp_select_ex(self.H, self.G, self.n, gamma, min_budget, self.ws, self.ws_bytes,
                      self.row_ptr, self.col_idx, self.stats_buf if with_stats else None, stream,
-                     vs_mode, qa_mode, max_budget)
+                     vs_mode, qa_mode, max_budget, block_size=self.b)
 
     def attn(self, q, k, v, out, stream=None):
         if self.layout is not None:
             fp_sparse_attn_ex(q, k, v, out, self.heads, self.kv_heads, self.n, self.layout,
-                              self.row_ptr, self.col_idx, self.ws, self.ws_bytes, stream)
+                              self.row_ptr, self.col_idx, self.ws, self.ws_bytes, stream,
+                              block_size=self.b)
             return
         fp_sparse_attn(q, k, v, out, self.H, self.G, self.n, self.row_ptr, self.col_idx, self.ws,
-                       self.ws_bytes, stream)
+                       self.ws_bytes, stream, block_size=self.b)
 
     def dense(self, q, k, v, out, stream=None):
         if self.layout is not None:
             fp_dense_causal_attn_ex(q, k, v, out, self.heads, self.kv_heads, self.n, self.layout,
-                                    self.ws, self.ws_bytes, stream)
+                                    self.ws, self.ws_bytes, stream, block_size=self.b)
             return
-        fp_dense_causal_attn(q, k, v, out, self.H, self.G, self.n, self.ws, self.ws_bytes, stream)
+        fp_dense_causal_attn(q, k, v, out, self.H, self.G, self.n, self.ws, self.ws_bytes, stream,
+                             block_size=self.b)
 
     def layer(self, q, k, v, out, gamma=0.95, tau=0.1, min_budget=0, stream=None):
         self.plan(q, k, tau, stream)
@@ -345,7 +349,7 @@ class FlexPrefill:
     def debug(self):
         """Copies of the workspace intermediates (torch CPU tensors)."""
         import torch
-        d = fp_debug_view(self.ws, self.H, self.G, self.n)
+        d = fp_debug_view(self.ws, self.H, self.G, self.n, block_size=self.b)
         base = self.ws.data_ptr()
         H, G, n, nb, tri = self.H, self.G, self.n, self.nb, self.cap
 

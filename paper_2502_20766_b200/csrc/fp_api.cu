@@ -44,9 +44,12 @@ bool make_tile_map(CUtensorMap* map, const void* base, const TLayout& t, int n, 
 static fp_status check_shape(int heads, int kv_heads, int seq_len, int head_dim, int block_size) {
   if (heads <= 0 || kv_heads <= 0 || seq_len <= 0) return FP_ERR_SHAPE;
   if (heads % kv_heads != 0) return FP_ERR_SHAPE;
-  if (head_dim != 128 || block_size != 128) return FP_ERR_SHAPE;
-  if (seq_len < block_size) return FP_ERR_SHAPE;  // ragged n allowed (A26), n >= b (A13)
-  if (seq_len > (1 << 20)) return FP_ERR_SHAPE;  // bitmap / index capacity limit
+  if (head_dim != 128 || (block_size != 128 && block_size != 64)) return FP_ERR_SHAPE;
+  // ragged n allowed (A26); n >= b (A13) and n >= 128 (the representative
+  // passes read one 128-row tile; with b = 64 its last 64 rows are Q^)
+  if (seq_len < 128) return FP_ERR_SHAPE;
+  // bitmap / index capacity limit: nb <= 8192 blocks
+  if (seq_len > (block_size == 64 ? (1 << 19) : (1 << 20))) return FP_ERR_SHAPE;
   return FP_OK;
 }
 
@@ -99,7 +102,7 @@ extern "C" {
 
 size_t fp_workspace_bytes(int heads, int kv_heads, int seq_len, int head_dim, int block_size) {
   if (check_shape(heads, kv_heads, seq_len, head_dim, block_size) != FP_OK) return 0;
-  return ws_layout(make_shape(heads, kv_heads, seq_len)).total;
+  return ws_layout(make_shape(heads, kv_heads, seq_len, block_size)).total;
 }
 
 fp_status fp_layout_bhsd(int batch, int heads, int kv_heads, int seq_len, fp_layout* out) {
@@ -154,7 +157,7 @@ fp_status fp_plan_ex(const void* q, const void* k, int heads, int kv_heads, int 
   Layout lay;
   if ((st = to_layout(layout, heads, kv_heads, seq_len, &lay))) return st;
   if (!aligned16(q) || !aligned16(k) || !aligned16(ws)) return FP_ERR_ALIGN;
-  const Shape s = make_shape(lay.batch * heads, lay.batch * kv_heads, seq_len);
+  const Shape s = make_shape(lay.batch * heads, lay.batch * kv_heads, seq_len, block_size);
   const WsLayout L = ws_layout(s);
   if (ws_bytes < L.total) return FP_ERR_WORKSPACE;
   if ((st = check_device())) return st;
@@ -186,7 +189,7 @@ fp_status fp_select_ex(int heads, int kv_heads, int seq_len, int head_dim, int b
   if (opt.vs_mode < 0 || opt.vs_mode > 1 || opt.qa_mode < 0 || opt.qa_mode > 1 || opt.max_budget < 0)
     return FP_ERR_RANGE;
   if (!aligned16(ws)) return FP_ERR_ALIGN;
-  const Shape s = make_shape(heads, kv_heads, seq_len);
+  const Shape s = make_shape(heads, kv_heads, seq_len, block_size);
   const WsLayout L = ws_layout(s);
   if (ws_bytes < L.total) return FP_ERR_WORKSPACE;
   if ((st = check_device())) return st;
@@ -211,7 +214,7 @@ static fp_status attn_common(const void* q, const void* k, const void* v, void* 
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return FP_ERR_ALIGN;
   (void)ws_bytes;
   if ((st = check_device())) return st;
-  const Shape s = make_shape(lay.batch * heads, lay.batch * kv_heads, seq_len);
+  const Shape s = make_shape(lay.batch * heads, lay.batch * kv_heads, seq_len, block_size);
   const WsLayout L = ws_layout(s);
   CUtensorMap qm, km, vm;
   if (!make_tile_map(&qm, q, lay.q, seq_len, lay.batch) ||
@@ -283,7 +286,7 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
   // two workspace slots (the full-layer workspace holds at least two).
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   const int g = heads / kv_heads;
-  const size_t n = (size_t)seq_len, nb = (n + 127) / 128, cap = nb * (nb + 1) / 2;
+  const size_t n = (size_t)seq_len, nb = (n + block_size - 1) / block_size, cap = nb * (nb + 1) / 2;
   const size_t qb_bytes = (size_t)g * n * 128 * 2, kv_bytes = n * 128 * 2;
   const size_t slot = align256(fp_workspace_bytes(g, 1, seq_len, head_dim, block_size));
   const int nslots = (kv_heads > 1 && ws_bytes >= 2 * slot) ? 2 : 1;
@@ -375,7 +378,7 @@ fp_status fp_debug_view(const void* ws, int heads, int kv_heads, int seq_len, in
   if (!ws || !out) return FP_ERR_NULL;
   fp_status st = check_shape(heads, kv_heads, seq_len, head_dim, block_size);
   if (st) return st;
-  const WsLayout L = ws_layout(make_shape(heads, kv_heads, seq_len));
+  const WsLayout L = ws_layout(make_shape(heads, kv_heads, seq_len, block_size));
   void* w = const_cast<void*>(ws);
   out->a_v = wsp<float>(w, L.a_v);
   out->a_s = wsp<float>(w, L.a_s);

@@ -469,6 +469,9 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
                            const void* const* peer_o, int n_peer, cudaStream_t st);
+cudaError_t launch_attn_b64(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
+                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+                            const int32_t* row_ptr, const int32_t* col_idx, cudaStream_t st);
 cudaError_t launch_attn_v9(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
@@ -495,6 +498,13 @@ cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layou
                         const void* const* peer_o, int n_peer, cudaStream_t st) {
   (void)L;
   (void)ws;
+  if (s.b != 128) {
+    // dense causal attention does not depend on the block size: the 128 kernel
+    if (dense) return launch_attn(make_shape(s.H, s.G, s.n, 128), L, ws, lay, qmap, kmap, vmap, o,
+                                  row_ptr, col_idx, dense, peer_o, n_peer, st);
+    if (n_peer > 0) return cudaErrorNotSupported;
+    return launch_attn_b64(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, st);
+  }
   if (FP_ATTN_VERSION == 8)
     return launch_attn_v8(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, peer_o, n_peer, st);
   if (n_peer > 0) return cudaErrorNotSupported;  // the fused output exchange is v8's

@@ -13,21 +13,26 @@ constexpr int kChunkTilesMax = 8;  // key tiles (128 keys) per representative-pa
 
 struct Shape {
   int H, G, n, nb, nchunks, g;  // flattened heads (batch * heads per sequence); g = H / G
+  int b, lb;                    // block_size (64 or 128) and log2(b)
+  int nt;                       // 128-key tiles of the representative passes: ceil(n / 128)
   int ct;                       // key tiles per representative-pass CTA
   long long tri;                // nb (nb + 1) / 2
 };
 
-inline Shape make_shape(int heads, int kv_heads, int seq_len) {
+inline Shape make_shape(int heads, int kv_heads, int seq_len, int block = 128) {
   Shape s;
   s.H = heads;
   s.G = kv_heads;
   s.n = seq_len;
-  s.nb = (seq_len + 127) / 128;  // ragged n: the last block is partial (A26)
+  s.b = block;
+  s.lb = block == 64 ? 6 : 7;
+  s.nb = (seq_len + block - 1) / block;  // ragged n: the last block is partial (A26)
+  s.nt = (seq_len + 127) / 128;
   // largest chunk (<= 8 tiles) that still gives >= 2 CTAs per SM of the
   // 148-SM B200 for the representative passes (short sequences: smaller chunks)
   s.ct = kChunkTilesMax;
-  while (s.ct > 1 && (long long)((s.nb + s.ct - 1) / s.ct) * heads < 2 * 148) s.ct >>= 1;
-  s.nchunks = (s.nb + s.ct - 1) / s.ct;
+  while (s.ct > 1 && (long long)((s.nt + s.ct - 1) / s.ct) * heads < 2 * 148) s.ct >>= 1;
+  s.nchunks = (s.nt + s.ct - 1) / s.ct;
   s.g = heads / kv_heads;
   s.tri = (long long)s.nb * (s.nb + 1) / 2;
   return s;
@@ -38,7 +43,7 @@ struct WsLayout {
   size_t m_part, l_part;     // fp32 [H][nchunks][128]  pass-1 partial row max / sum (log2 domain)
   size_t m_row, il_row;      // fp32 [H][128]           combined row max, 1/row sum
   size_t a_v, a_s;           // fp32 [H][n]
-  size_t as_part;            // fp32 [H][nb][256]       per-key-tile slash partials
+  size_t as_part;            // fp32 [H][nt][256]       per-key-tile slash partials
   size_t a_hat, a_bar, As;   // fp32 [H][nb]
   size_t k_bar;              // fp32 [G][nb][128]
   size_t q_bar;              // fp32 [H][nb][128]
@@ -78,7 +83,7 @@ inline WsLayout ws_layout(const Shape& s) {
   L.il_row = take(H * 128 * 4);
   L.a_v = take(H * n * 4);
   L.a_s = take(H * n * 4);
-  L.as_part = take(H * nb * 256 * 4);
+  L.as_part = take(H * (size_t)s.nt * 256 * 4);
   L.a_hat = take(H * nb * 4);
   L.a_bar = take(H * nb * 4);
   L.As = take(H * nb * 4);

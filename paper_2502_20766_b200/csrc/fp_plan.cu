@@ -108,7 +108,8 @@ __device__ float block_max(float v, float* red) {
 template <int PASS>
 __global__ void __launch_bounds__(kRepThreads, 1)
     rep_pass(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-             int H, int G, int Hp, int Gp, int n, int nb, int nchunks, int ct, float scale_log2,
+             int H, int G, int Hp, int Gp, int n, int nb, int nt, int bsz, int nchunks, int ct,
+             float scale_log2,
              float* __restrict__ m_part,
              float* __restrict__ l_part, const float* __restrict__ m_row,
              const float* __restrict__ il_row, float* __restrict__ k_bar, float* __restrict__ a_v,
@@ -125,7 +126,11 @@ __global__ void __launch_bounds__(kRepThreads, 1)
   const int chunk = blockIdx.x, h = blockIdx.y;
   const int g = h / (H / G);
   const int t0 = chunk * ct;
-  const int ntile = min(ct, nb - t0);
+  const int ntile = min(ct, nt - t0);
+  // block_size b = 64: Q^ is the last 64 rows, i.e. rows r >= 64 of the
+  // 128-row representative tile (p_r = n - 128 + r either way)
+  const int r_lo = 128 - bsz;
+  const float inv_b = 1.0f / (float)bsz;
   const bool do_kbar = (PASS == 1) && (h % (H / G) == 0);
 
   if (warp_id() == 0) tmem_alloc(&sm.tmem_base, 256);
@@ -223,9 +228,15 @@ __global__ void __launch_bounds__(kRepThreads, 1)
         sm.red[tid] = a0 + a1;
         __syncthreads();
         // ragged last block: zero-filled rows past n, mean over the actual rows (A26)
-        if (tid < 128)
-          k_bar[((size_t)g * nb + tile) * 128 + tid] =
-              (sm.red[tid] + sm.red[tid + 128]) / (float)min(128, n - tile * 128);
+        if (bsz == 128) {
+          if (tid < 128)
+            k_bar[((size_t)g * nb + tile) * 128 + tid] =
+                (sm.red[tid] + sm.red[tid + 128]) / (float)min(128, n - tile * 128);
+        } else {  // two 64-key blocks per tile: thread halves are the blocks
+          const int kb = 2 * tile + (tid >> 7);
+          const int cnt = min(64, n - kb * 64);
+          if (cnt > 0) k_bar[((size_t)g * nb + kb) * 128 + (tid & 127)] = sm.red[tid] / (float)cnt;
+        }
       }
     } else {
       // lane = key j_local, columns = rep rows r = half*64 .. half*64+63
@@ -233,18 +244,23 @@ __global__ void __launch_bounds__(kRepThreads, 1)
       const int j = tile * 128 + jl;
       float cs[4] = {0.f, 0.f, 0.f, 0.f};
       float* Trow = T + jl * kTStride + half * 64;
+      if (half * 64 >= r_lo) {
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const int r = half * 64 + c;
-        float p = fast_exp2(fmaf(__uint_as_float(v[c]), scale_log2, -sm.m_row[r])) * sm.il_row[r];
-        if (last && jl > lim + r) p = 0.f;
-        cs[c & 3] += p;
-        Trow[c] = p;
+        for (int c = 0; c < 64; ++c) {
+          const int r = half * 64 + c;
+          float p = fast_exp2(fmaf(__uint_as_float(v[c]), scale_log2, -sm.m_row[r])) * sm.il_row[r];
+          if (last && jl > lim + r) p = 0.f;
+          cs[c & 3] += p;
+          Trow[c] = p;
+        }
+      } else {  // rows outside Q^ (b = 64): no probability mass
+#pragma unroll
+        for (int c = 0; c < 64; ++c) Trow[c] = 0.f;
       }
       sm.red[half * 128 + jl] = (cs[0] + cs[1]) + (cs[2] + cs[3]);
       __syncthreads();
       if (tid < 128 && tile * 128 + tid < n)
-        a_v[(size_t)h * n + tile * 128 + tid] = (sm.red[tid] + sm.red[128 + tid]) * (1.0f / 128.0f);
+        a_v[(size_t)h * n + tile * 128 + tid] = (sm.red[tid] + sm.red[128 + tid]) * inv_b;
       (void)j;
       // slash partials: diagonal delta = r - jl in [-127, 127], one per thread;
       // offset o = p_r - j = (n - 128 - tile*128) + delta
@@ -261,7 +277,7 @@ __global__ void __launch_bounds__(kRepThreads, 1)
           tp += 2 * (kTStride + 1);
         }
         if (q < q1) s0 += tp[0];
-        as_part[((size_t)h * nb + tile) * 256 + dl + 127] = s0 + s1;
+        as_part[((size_t)h * nt + tile) * 256 + dl + 127] = s0 + s1;
       }
     }
     tc_fence_before();
@@ -309,7 +325,7 @@ __global__ void rep_stats(int nchunks, const float* __restrict__ m_part,
 }
 
 // a_s[o] = (sum of the overlapping per-tile diagonal partials) / b  (A9)
-__global__ void slash_combine(int n, int nb, const float* __restrict__ as_part,
+__global__ void slash_combine(int n, int nt, float inv_b, const float* __restrict__ as_part,
                               float* __restrict__ a_s) {
   const int h = blockIdx.y;
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
@@ -318,22 +334,22 @@ __global__ void slash_combine(int n, int nb, const float* __restrict__ as_part,
   int kt_hi = (q + 127) >= 0 ? (q + 127) / 128 : -1;
   float s = 0.f;
   for (int kt = kt_hi - 1; kt <= kt_hi; ++kt) {  // ascending kt
-    if (kt < 0 || kt >= nb) continue;
+    if (kt < 0 || kt >= nt) continue;
     const int delta = 128 * kt - q;
     if (delta < -127 || delta > 127) continue;
-    s += as_part[((size_t)h * nb + kt) * 256 + delta + 127];
+    s += as_part[((size_t)h * nt + kt) * 256 + delta + 127];
   }
-  a_s[(size_t)h * n + o] = s * (1.0f / 128.0f);
+  a_s[(size_t)h * n + o] = s * inv_b;
 }
 
 // a_hat[kb] = sum_{j in kb} a_v[j] (A2) and As[D] = sum_{o in block D} a_s[o] (A12)
-__global__ void block_sums(int n, int nb, const float* __restrict__ a_v,
+__global__ void block_sums(int n, int nb, int b, const float* __restrict__ a_v,
                            const float* __restrict__ a_s, float* __restrict__ a_hat,
                            float* __restrict__ As) {
   __shared__ float red[33];
   const int kb = blockIdx.x, h = blockIdx.y;
-  const size_t i = (size_t)h * n + (size_t)kb * 128 + threadIdx.x;
-  const bool in = kb * 128 + (int)threadIdx.x < n;  // ragged last block (A26)
+  const size_t i = (size_t)h * n + (size_t)kb * b + threadIdx.x;
+  const bool in = (int)threadIdx.x < b && kb * b + (int)threadIdx.x < n;  // ragged last block (A26)
   float sv = block_sum<128>(in ? a_v[i] : 0.f, red);
   float ss = block_sum<128>(in ? a_s[i] : 0.f, red);
   if (threadIdx.x == 0) {
@@ -346,7 +362,7 @@ __global__ void block_sums(int n, int nb, const float* __restrict__ a_v,
 constexpr int kPatThreads = 256;
 __global__ void __launch_bounds__(kPatThreads) pattern_kernel(
     const __nv_bfloat16* __restrict__ q, TLayout ql, const float* __restrict__ k_bar,
-    const float* __restrict__ a_hat, int H, int G, int n, int nb, float scale, float tau,
+    const float* __restrict__ a_hat, int H, int G, int n, int nb, int b, float scale, float tau,
     float* __restrict__ a_bar, int32_t* __restrict__ pattern_ws, float* __restrict__ jsd_ws,
     int32_t* __restrict__ pattern_out, float* __restrict__ jsd_out) {
   extern __shared__ float psm[];  // qbar[128] | logits[nb] | red[33]
@@ -356,10 +372,11 @@ __global__ void __launch_bounds__(kPatThreads) pattern_kernel(
   const int h = blockIdx.x, g = h / (H / G);
   const int tid = threadIdx.x;
   if (tid < 128) {
-    const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + toff(ql, h, n - 128) + tid;
+    // q_bar = avgpool(Q^), Q^ = the last b query rows
+    const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + toff(ql, h, n - b) + tid;
     float acc = 0.f;
-    for (int r = 0; r < 128; ++r) acc += bf16_to_f32(qh[(size_t)r * ql.rs]);
-    qbar[tid] = acc * (1.0f / 128.0f);
+    for (int r = 0; r < b; ++r) acc += bf16_to_f32(qh[(size_t)r * ql.rs]);
+    qbar[tid] = acc / (float)b;
   }
   __syncthreads();
   const int w = warp_id(), ln = lane_id();
@@ -402,12 +419,12 @@ __global__ void __launch_bounds__(kPatThreads) pattern_kernel(
 // avg-pooled queries of Query-Aware heads (Alg. 4 line 1)
 // (a ragged last block averages over its actual rows, A26)
 __global__ void qbar_kernel(const __nv_bfloat16* __restrict__ q, TLayout ql,
-                            const int32_t* __restrict__ pattern, int n, int nb,
+                            const int32_t* __restrict__ pattern, int n, int nb, int b,
                             float* __restrict__ q_bar) {
   const int qb = blockIdx.x, h = blockIdx.y;
   if (pattern[h] != 1) return;
-  const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + toff(ql, h, qb * 128) + threadIdx.x;
-  const int cnt = min(128, n - qb * 128);
+  const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + toff(ql, h, qb * b) + threadIdx.x;
+  const int cnt = min(b, n - qb * b);
   float acc = 0.f;
 #pragma unroll 8
   for (int r = 0; r < cnt; ++r) acc += bf16_to_f32(qh[(size_t)r * ql.rs]);
@@ -500,27 +517,28 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
   dim3 grid(s.nchunks, s.H);
   (void)k;
   const int Hp = lay.q.per, Gp = lay.k.per;
-  rep_pass<1><<<grid, kRepThreads, sm1, st>>>(qmap, kmap, s.H, s.G, Hp, Gp, s.n, s.nb, s.nchunks, s.ct, scale_log2,
+  rep_pass<1><<<grid, kRepThreads, sm1, st>>>(qmap, kmap, s.H, s.G, Hp, Gp, s.n, s.nb, s.nt, s.b, s.nchunks, s.ct, scale_log2,
                                               m_part, l_part, m_row, il_row,
                                               wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_v),
                                               wsp<float>(ws, L.as_part));
   rep_stats<<<s.H, 128, 0, st>>>(s.nchunks, m_part, l_part, m_row, il_row);
-  rep_pass<2><<<grid, kRepThreads, sm2, st>>>(qmap, kmap, s.H, s.G, Hp, Gp, s.n, s.nb, s.nchunks, s.ct, scale_log2,
+  rep_pass<2><<<grid, kRepThreads, sm2, st>>>(qmap, kmap, s.H, s.G, Hp, Gp, s.n, s.nb, s.nt, s.b, s.nchunks, s.ct, scale_log2,
                                               m_part, l_part, m_row, il_row,
                                               wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_v),
                                               wsp<float>(ws, L.as_part));
-  slash_combine<<<dim3((s.n + 255) / 256, s.H), 256, 0, st>>>(s.n, s.nb, wsp<float>(ws, L.as_part),
+  slash_combine<<<dim3((s.n + 255) / 256, s.H), 256, 0, st>>>(s.n, s.nt, 1.0f / (float)s.b,
+                                                              wsp<float>(ws, L.as_part),
                                                               wsp<float>(ws, L.a_s));
-  block_sums<<<dim3(s.nb, s.H), 128, 0, st>>>(s.n, s.nb, wsp<float>(ws, L.a_v),
+  block_sums<<<dim3(s.nb, s.H), 128, 0, st>>>(s.n, s.nb, s.b, wsp<float>(ws, L.a_v),
                                               wsp<float>(ws, L.a_s), wsp<float>(ws, L.a_hat),
                                               wsp<float>(ws, L.As));
   const size_t psm = (128 + (size_t)s.nb + 33) * 4;
   pattern_kernel<<<s.H, kPatThreads, psm, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(q), lay.q, wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_hat),
-      s.H, s.G, s.n, s.nb, scale, tau, wsp<float>(ws, L.a_bar), wsp<int32_t>(ws, L.pattern),
+      s.H, s.G, s.n, s.nb, s.b, scale, tau, wsp<float>(ws, L.a_bar), wsp<int32_t>(ws, L.pattern),
       wsp<float>(ws, L.jsd), pattern_out, jsd_out);
   qbar_kernel<<<dim3(s.nb, s.H), 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
-                                               wsp<int32_t>(ws, L.pattern), s.n, s.nb,
+                                               wsp<int32_t>(ws, L.pattern), s.n, s.nb, s.b,
                                                wsp<float>(ws, L.q_bar));
   const int nt = (s.nb + kPT - 1) / kPT;
   pooled_logits<<<dim3(nt, nt, s.H), 256, 0, st>>>(wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar),

@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kRowThreads) topmass_rows(
 // vertical-block and slash-diagonal bitmaps of VS heads (A10, reading R1)
 __global__ void build_lines(const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_v,
                             const int32_t* __restrict__ sel_s, const int32_t* __restrict__ sel_count,
-                            int n, int nb, int nbw, int vs_mode, uint32_t* __restrict__ vbits,
+                            int n, int nb, int nbw, int vs_mode, int lb, uint32_t* __restrict__ vbits,
                             uint32_t* __restrict__ dbits) {
   extern __shared__ uint32_t bsm[];  // V[nbw] | D[nbw]
   const int h = blockIdx.x;
@@ -501,16 +501,16 @@ __global__ void build_lines(const int32_t* __restrict__ pattern, const int32_t* 
     const int32_t* sv = sel_v + (size_t)h * n;
     const int32_t* ss = sel_s + (size_t)h * n;
     for (int i = threadIdx.x; i < kv; i += blockDim.x) {
-      const int kb = vs_mode ? sv[i] : (sv[i] >> 7);
+      const int kb = vs_mode ? sv[i] : (sv[i] >> lb);
       atomicOr(&V[kb >> 5], 1u << (kb & 31));
     }
     for (int i = threadIdx.x; i < ks; i += blockDim.x) {
       const int o = ss[i];
-      const int d = vs_mode ? o : (o >> 7);
+      const int d = vs_mode ? o : (o >> lb);
       atomicOr(&Dg[d >> 5], 1u << (d & 31));
       // R1: offset o crosses diagonals o/b and o/b + 1 (unless aligned);
       // R2 (vs_mode 1): the offset group [d b, (d+1) b) covers d and d + 1
-      if ((vs_mode || (o & 127)) && d + 1 < nb) atomicOr(&Dg[(d + 1) >> 5], 1u << ((d + 1) & 31));
+      if ((vs_mode || (o & ((1 << lb) - 1))) && d + 1 < nb) atomicOr(&Dg[(d + 1) >> 5], 1u << ((d + 1) & 31));
     }
   }
   __syncthreads();
@@ -769,10 +769,11 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
   build_lines<<<s.H, 1024, 2 * L.nbw * 4, st>>>(pat, wsp<int32_t>(ws, L.sel_v),
                                                 wsp<int32_t>(ws, L.sel_s),
                                                 wsp<int32_t>(ws, L.sel_count), s.n, s.nb, L.nbw,
-                                                opt.vs_mode, wsp<uint32_t>(ws, L.vbits),
+                                                opt.vs_mode, s.lb, wsp<uint32_t>(ws, L.vbits),
                                                 wsp<uint32_t>(ws, L.dbits));
-  const int min_blocks = (min_budget + 127) / 128;
-  const int max_blocks = (opt.max_budget + 127) / 128;
+  // A12 / f2: budgets in tokens -> key blocks of this block size
+  const int min_blocks = (min_budget + s.b - 1) / s.b;
+  const int max_blocks = (opt.max_budget + s.b - 1) / s.b;
   const dim3 rg((s.nb + kAsmWarps - 1) / kAsmWarps, s.H);
   assemble_rows<<<rg, kAsmWarps * 32, kAsmWarps * 2 * L.nbw * 4, st>>>(
       pat, wsp<uint32_t>(ws, L.vbits), wsp<uint32_t>(ws, L.dbits), wsp<int32_t>(ws, L.sel_qa),

@@ -21,14 +21,14 @@ def to_torch_bf16(bits, device="cuda"):
 
 
 def run_gpu(fp, w, q_bits, k_bits, v_bits, gamma=None, tau=None, min_budget=None, dense=False,
-            want_out=True, vs_mode=0, qa_mode=0, max_budget=0):
+            want_out=True, vs_mode=0, qa_mode=0, max_budget=0, block_size=128):
     """Run plan -> select -> attn through the binding; return host copies."""
     import torch
     gamma = w.gamma if gamma is None else gamma
     tau = w.tau if tau is None else tau
     min_budget = w.min_budget if min_budget is None else min_budget
     q, k, v = (to_torch_bf16(x) for x in (q_bits, k_bits, v_bits))
-    fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len)
+    fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len, block_size=block_size)
     fpl.plan(q, k, tau)
     fpl.select(gamma, min_budget, vs_mode=vs_mode, qa_mode=qa_mode, max_budget=max_budget)
     out = torch.empty_like(q)

@@ -43,7 +43,15 @@ def test_workspace_and_capacity(lib):
     for bad in [(32, 7, 32768), (32, 8, 100), (32, 8, 64), (0, 1, 2048)]:
         assert fp.fp_workspace_bytes(*bad) == 0
     assert fp.fp_workspace_bytes(4, 1, 2048, head_dim=64) == 0
-    assert fp.fp_workspace_bytes(4, 1, 2048, block_size=64) == 0
+    # block_size 64 (next row f3): supported; other sizes are not
+    b64 = fp.fp_workspace_bytes(4, 1, 2048, block_size=64)
+    assert b64 > fp.fp_workspace_bytes(4, 1, 2048) > 0  # 2x the blocks: larger maps
+    for bad_b in (32, 96, 256):
+        assert fp.fp_workspace_bytes(4, 1, 2048, block_size=bad_b) == 0
+    assert fp.fp_col_idx_capacity(131072, 64) == 2048 * 2049 // 2
+    assert fp.fp_workspace_bytes(4, 1, 100, block_size=64) == 0       # n < 128
+    assert fp.fp_workspace_bytes(1, 1, (1 << 19) + 64, block_size=64) == 0  # nb > 8192
+    assert fp.fp_workspace_bytes(1, 1, 1 << 19, block_size=64) > 0
 
 
 def test_validation_codes_without_device(lib):

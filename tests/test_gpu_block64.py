@@ -1,0 +1,123 @@
+"""Next row f3: block_size = 64 (the paper's Triton block
+size ablation). The whole path runs with 64-token blocks: Q^ is the
+last 64 query rows, pooled estimates and line rasterisation use
+64-blocks, and the attention computes exactly the selected 64 x 64 blocks
+(fp_attn64.cu: coarse 128 x 128 tensor-core tiles with per-quadrant masks).
+Parity against the float64 oracle run with b = 64."""
+import numpy as np
+import pytest
+
+import oracle
+from synth import gen
+from synth.configs import Workload
+from tests import parity
+from tests.test_gpu_parity import (MAX_ABS, MEAN_ABS, _check_attn_stagewise, _check_plan,
+                                   _check_select_stagewise, _oracle_plans, full_parity)
+
+pytestmark = pytest.mark.gpu
+B = 64
+
+
+@pytest.fixture(scope="module")
+def fp():
+    import paper_2502_20766_b200 as m
+    m.load_library()
+    return m
+
+
+@pytest.mark.parametrize("heads,kv,n,gamma,min_budget", [
+    (4, 1, 2048, 0.9, 0),        # C1 layout: 32 blocks of 64
+    (8, 2, 2085, 0.95, 1024),    # ragged: last 64-block holds 37 rows; min budget 16 blocks
+    (4, 2, 1000, 0.9, 0),        # 16 blocks (last 40 rows): the last coarse tile has no row B
+    (4, 1, 128, 0.9, 0),         # two blocks, one coarse tile
+])
+def test_block64_full_parity(fp, heads, kv, n, gamma, min_budget):
+    w = Workload(f"b64-{n}", heads, kv, n, gamma, 0.1, min_budget, 90 + n % 89)
+    res = full_parity(fp, w, b=B)
+    nb = -(-n // B)
+    assert res["row_ptr"].shape[1] == nb + 1
+    assert all(s_["nnz_blocks"] >= 2 * nb - 1 for s_ in res["stats"])  # forced blocks
+
+
+def test_block64_both_patterns_and_finer_sets(fp):
+    """the C1 workload selects both patterns at b = 64 too, and the 64-block
+    sets are no coarser than the 128-block ones (each selected 128-block of
+    the b = 128 run is covered by the b = 64 selection's 64-blocks at >= 1/4)."""
+    w = Workload("b64-c1", 4, 1, 2048, 0.9, 0.1, 0, 101)
+    q, k, v = gen.make_layer_bits(w)
+    r64 = parity.run_gpu(fp, w, q, k, v, block_size=64)
+    assert set(r64["pattern"].tolist()) == {0, 1}
+    nb = 32
+    for h in range(w.heads):
+        M = parity.csr_mask(r64["row_ptr"][h], r64["col_idx"][h], nb)
+        assert parity.csr_rows_sorted(r64["row_ptr"][h], r64["col_idx"][h], nb)
+        assert M.sum() < nb * (nb + 1) // 2  # sparse
+
+
+@pytest.mark.parametrize("n,density,seed", [(2048, 0.3, 1), (2085, 0.5, 2), (4096, 0.15, 3)])
+def test_block64_attention_random_masks(fp, n, density, seed):
+    """fp_sparse_attn on random 64-block CSRs (each row: block 0, its diagonal,
+    random others): every quadrant combination of the coarse tiles, ragged n."""
+    import torch
+    H, G = 4, 2
+    w = Workload(f"b64-rand-{n}", H, G, n, 0.9, 0.1, 0, 120 + seed)
+    q, k, v = gen.make_layer_bits(w)
+    Q, K, V = parity.oracle_inputs(q, k, v)
+    nb = -(-n // B)
+    rng = np.random.default_rng(seed)
+    masks, rp, ci = [], [], []
+    cap = nb * (nb + 1) // 2
+    for h in range(H):
+        M = np.tril(rng.random((nb, nb)) < density)
+        M[:, 0] = True
+        M[np.arange(nb), np.arange(nb)] = True
+        masks.append(M)
+        r = np.zeros(nb + 1, np.int32)
+        c = np.zeros(cap, np.int32)
+        off = 0
+        for qb in range(nb):
+            ks = np.nonzero(M[qb, : qb + 1])[0]
+            c[off: off + len(ks)] = ks
+            off += len(ks)
+            r[qb + 1] = off
+        rp.append(r)
+        ci.append(c)
+    qt, kt, vt = (parity.to_torch_bf16(x) for x in (q, k, v))
+    rpt = torch.from_numpy(np.stack(rp)).cuda()
+    cit = torch.from_numpy(np.stack(ci)).cuda()
+    out = torch.zeros_like(qt)
+    fp.fp_sparse_attn(qt, kt, vt, out, H, G, n, rpt, cit, block_size=B)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    for h in range(H):
+        ref = oracle.sparse_attention(Q[h], K[h * G // H], V[h * G // H], masks[h], B)
+        d = np.abs(got[h] - ref)
+        assert d.max() <= MAX_ABS and d.mean() <= MEAN_ABS, (h, d.max(), d.mean())
+
+
+def test_block64_gamma_one_is_dense(fp):
+    """gamma >= 1 selects every causal 64-block: the output is dense causal
+    attention (oracle), and the layer's dense kernel agrees."""
+    w = Workload("b64-g1", 4, 1, 1000, 1.0, 0.1, 0, 131)
+    q, k, v = gen.make_layer_bits(w)
+    Q, K, V = parity.oracle_inputs(q, k, v)
+    res = parity.run_gpu(fp, w, q, k, v, gamma=1.0, dense=True, block_size=B)
+    nb = -(-1000 // B)
+    assert np.all(res["row_ptr"][:, -1] == nb * (nb + 1) // 2)
+    for h in range(w.heads):
+        ref = oracle.dense_causal_attention(Q[h], K[0], V[0])
+        for key in ("out", "dense"):
+            d = np.abs(res[key][h] - ref)
+            assert d.max() <= MAX_ABS and d.mean() <= MEAN_ABS, (key, h, d.max())
+
+
+def test_block64_glm_group16_stagewise(fp):
+    """GQA group 16 (GLM-like) at b = 64 with min budget: plan, selection and
+    attention stage-wise on a subset of heads / q-blocks."""
+    w = Workload("b64-glm", 32, 2, 2048, 0.95, 0.1, 1024, 104)
+    q, k, v = gen.make_layer_bits(w)
+    Q, K, V = parity.oracle_inputs(q, k, v)
+    res = parity.run_gpu(fp, w, q, k, v, block_size=B)
+    _check_plan(w, res, _oracle_plans(w, Q, K, heads=[0, 1, 15, 16, 31], b=B))
+    _check_select_stagewise(w, res, w.gamma, w.min_budget, B)
+    _check_attn_stagewise(w, res, Q, K, V, qblocks=[0, 1, 7, 15, 16, 31], b=B)

@@ -27,9 +27,9 @@ def fp():
     return m
 
 
-def _oracle_plans(w, Q, K, heads=None):
+def _oracle_plans(w, Q, K, heads=None, b=128):
     hs = range(w.heads) if heads is None else heads
-    return {h: oracle.plan_head(Q[h], K[h * w.kv_heads // w.heads], 128, w.tau) for h in hs}
+    return {h: oracle.plan_head(Q[h], K[h * w.kv_heads // w.heads], b, w.tau) for h in hs}
 
 
 def _check_plan(w, res, plans):
@@ -42,9 +42,9 @@ def _check_plan(w, res, plans):
             assert rel <= 1e-4 and small <= 1e-7, (h, key, rel, small)
 
 
-def _check_select_stagewise(w, res, gamma, min_budget):
+def _check_select_stagewise(w, res, gamma, min_budget, b=128):
     dbg = res["dbg"]
-    nb = -(-w.seq_len // 128)
+    nb = -(-w.seq_len // b)
     for h in range(w.heads):
         pat = res["pattern"][h]
         cnt = dbg["sel_count"][h]
@@ -65,7 +65,7 @@ def _check_select_stagewise(w, res, gamma, min_budget):
         # CSR bit-exact vs oracle O6-O9 on the GPU's sets and fp32 scores
         rp, ci = res["row_ptr"][h], res["col_idx"][h]
         assert parity.csr_rows_sorted(rp, ci, nb)
-        M0, M = parity.stagewise_mask(pat, dbg, h, w.seq_len, gamma, min_budget)
+        M0, M = parity.stagewise_mask(pat, dbg, h, w.seq_len, gamma, min_budget, b)
         assert np.array_equal(parity.csr_mask(rp, ci, nb), M), h
         pre = oracle.add_forced(M0).sum(axis=1)
         assert np.array_equal(dbg["row_nnz_pre"][h], pre), h
@@ -73,13 +73,13 @@ def _check_select_stagewise(w, res, gamma, min_budget):
         assert st["nnz_blocks"] == M.sum() and st["pattern"] == pat
 
 
-def _check_attn_stagewise(w, res, Q, K, V, qblocks=None):
-    nb = -(-w.seq_len // 128)
+def _check_attn_stagewise(w, res, Q, K, V, qblocks=None, b=128):
+    nb = -(-w.seq_len // b)
     worst_max, worst_mean = 0.0, 0.0
     for h in range(w.heads):
         g = h * w.kv_heads // w.heads
         M = parity.csr_mask(res["row_ptr"][h], res["col_idx"][h], nb)
-        ref = oracle.sparse_attention(Q[h], K[g], V[g], M, 128, qblocks)
+        ref = oracle.sparse_attention(Q[h], K[g], V[g], M, b, qblocks)
         rows = ~np.isnan(ref[:, 0])
         d = np.abs(res["out"][h][rows] - ref[rows])
         worst_max = max(worst_max, float(d.max()))
@@ -94,21 +94,21 @@ def test_c1_full_parity(fp):
     assert set(res["pattern"].tolist()) == {0, 1}
 
 
-def full_parity(fp, w):
+def full_parity(fp, w, b=128):
     """plan, stage-wise selection and attention, end-to-end sets (borderline
-    rule) and outputs, and the dense kernel, all heads."""
+    rule) and outputs, and the dense kernel, all heads (block size b)."""
     q, k, v = gen.make_layer_bits(w)
     Q, K, V = parity.oracle_inputs(q, k, v)
-    res = parity.run_gpu(fp, w, q, k, v, dense=True)
-    plans = _oracle_plans(w, Q, K)
+    res = parity.run_gpu(fp, w, q, k, v, dense=True, block_size=b)
+    plans = _oracle_plans(w, Q, K, b=b)
     _check_plan(w, res, plans)
-    _check_select_stagewise(w, res, w.gamma, w.min_budget)
-    _check_attn_stagewise(w, res, Q, K, V)
+    _check_select_stagewise(w, res, w.gamma, w.min_budget, b)
+    _check_attn_stagewise(w, res, Q, K, V, b=b)
     # end-to-end: oracle from scratch, borderline rule
-    nb = -(-w.seq_len // 128)
+    nb = -(-w.seq_len // b)
     for h in range(w.heads):
         g = h * w.kv_heads // w.heads
-        o = oracle.flexprefill_head(Q[h], K[g], V[g], 128, w.gamma, w.tau, w.min_budget,
+        o = oracle.flexprefill_head(Q[h], K[g], V[g], b, w.gamma, w.tau, w.min_budget,
                                     with_output=False)
         cnt = res["dbg"]["sel_count"][h]
         if o["pattern"] == oracle.VS:
@@ -123,7 +123,7 @@ def full_parity(fp, w):
         # rows whose block lists match: outputs vs oracle output on the oracle's set
         Mg = parity.csr_mask(res["row_ptr"][h], res["col_idx"][h], nb)
         same = np.all(Mg == o["mask"], axis=1)
-        ref = oracle.sparse_attention(Q[h], K[g], V[g], o["mask"], 128, np.nonzero(same)[0])
+        ref = oracle.sparse_attention(Q[h], K[g], V[g], o["mask"], b, np.nonzero(same)[0])
         rows = ~np.isnan(ref[:, 0])
         if rows.any():
             d = np.abs(res["out"][h][rows] - ref[rows])

@@ -23,8 +23,8 @@ from synth import configs as C  # noqa: E402
 from synth import gen  # noqa: E402
 
 
-def useful_flops(nnz, nb):
-    return sum(4 * 128 * (128 * 128 * (int(x) - nb) + nb * 128 * 129 // 2) for x in nnz)
+def useful_flops(nnz, nb, b=128):
+    return sum(4 * 128 * (b * b * (int(x) - nb) + nb * b * (b + 1) // 2) for x in nnz)
 
 
 def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flush=None, opts=None):
@@ -53,6 +53,7 @@ def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flus
         fpl.select(w.gamma, w.min_budget, with_stats=False, **opts)
         fpl.attn(q, k, v, out)
 
+
     ms = timed(layer, steps, warmup)
     # the same layer replayed from one CUDA graph (no host launch gaps: short
     # sequences are launch-bound when timed eagerly)
@@ -80,7 +81,7 @@ def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flus
     torch.cuda.synchronize()
     attn_ms = a.elapsed_time(b)
     stats = fpl.stats()
-    nb = w.seq_len // 128
+    nb = fpl.nb
     nnz = [s_["nnz_blocks"] for s_ in stats]
     pats = [s_["pattern"] for s_ in stats]
     dms = timed(lambda: fpl.dense(q, k, v, out), max(2, steps // 2), 1) if dense else None
@@ -95,7 +96,8 @@ def measure(fp, torch, w, q, k, v, fpl, out, steps=5, warmup=2, dense=True, flus
         "density": float(np.sum(nnz)) / (len(nnz) * nb * (nb + 1) / 2),
         "qa_heads": int(np.sum(pats)), "vs_heads": int(len(pats) - np.sum(pats)),
         "budget_added": int(sum(s_["budget_added"] for s_ in stats)),
-        "attn_tflops_useful": useful_flops(nnz, nb) / (attn_ms / 1e3) / 1e12,
+        "block_size": fpl.b,
+        "attn_tflops_useful": useful_flops(nnz, nb, fpl.b) / (attn_ms / 1e3) / 1e12,
         "dense_tflops": (w.heads * 4 * 128 * w.seq_len * (w.seq_len + 1) / 2) / (dms / 1e3) / 1e12
         if dms else None,
     }
@@ -113,6 +115,12 @@ def points(which):
         for mb in (1024, 0):
             for g in C.C4_GAMMAS:
                 yield C.C4.with_(gamma=g, min_budget=mb), None
+    elif which == "b64":  # next row f3: block size 64 vs 128 on the same inputs
+        for bs in (128, 64):
+            for g in (0.9, 0.95):
+                yield C.C3.with_(gamma=g), {"block_size": bs}
+            for n in (8192, 32768):
+                yield C.C5_QWEN.with_(seq_len=n, name=f"{C.C5_QWEN.name}-{n // 1024}k"), {"block_size": bs}
     elif which == "c5short":
         for base in (C.C5_QWEN, C.C5_YI):
             for n in (4096, 8192, 16384):
@@ -134,7 +142,9 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     f = open(out_path, "a") if out_path else None
     for w, opts in points(which):
-        key = (w.heads, w.kv_heads, w.seq_len, w.seed)
+        bs = (opts or {}).pop("block_size", 128) if opts else 128
+        opts = opts or None
+        key = (w.heads, w.kv_heads, w.seq_len, w.seed, bs)
         if key not in cache:
             cache.clear()
             torch.cuda.empty_cache()
@@ -142,7 +152,7 @@ def main():
             qb, kb, vb = gen.make_layer_bits(w)
             q, k, v = (torch.from_numpy(x).view(torch.bfloat16).cuda() for x in (qb, kb, vb))
             del qb, kb, vb
-            fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len)
+            fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len, block_size=bs)
             cache[key] = (q, k, v, fpl, torch.empty_like(q))
             print(f"# generated {key} in {time.time() - t:.1f}s", file=sys.stderr, flush=True)
         q, k, v, fpl, out = cache[key]
