@@ -177,6 +177,25 @@ def oracle_sample(w, budget_s, nnz_per_head=None, heads=(0, None)):
             t_attn += time.perf_counter() - t
             blocks += int(masks[h][qb].sum())
         i += 1
+    # true attention coverage a_S(i) = sum_{j in S_i} softmax_j(q_i k_j / sqrt d) of the
+    # sampled rows (SURVEY §8(d) "per head"; the method guarantees gamma only on its
+    # estimates, reading A19), outside the timed region
+    cov = {}
+    for h in (hv, hq):
+        vals = []
+        for qb in [nb - 1, nb // 2, 1]:
+            rows = np.arange(qb * 128, qb * 128 + 128)
+            logits = q[h][rows] @ kk[: rows[-1] + 1].T / np.sqrt(128.0)
+            j = np.arange(rows[-1] + 1)
+            causal = j[None, :] <= rows[:, None]
+            logits = np.where(causal, logits, -np.inf)
+            pr = np.exp(logits - logits.max(axis=1, keepdims=True))
+            pr /= pr.sum(axis=1, keepdims=True)
+            sel = np.repeat(masks[h][qb, : qb + 1], 128)[: rows[-1] + 1]
+            vals.append((pr * sel[None, :]).sum(axis=1))
+        v_ = np.concatenate(vals)
+        cov[str(h)] = {"min": round(float(v_.min()), 4), "mean": round(float(v_.mean()), 4),
+                       "qblocks": [nb - 1, nb // 2, 1]}
     if nnz_per_head is None:
         total_blocks = (H / 2) * (masks[hv].sum() + masks[hq].sum())
     else:
@@ -189,6 +208,7 @@ def oracle_sample(w, budget_s, nnz_per_head=None, heads=(0, None)):
     return {
         "est_layer_s": est,
         "cores": cores,
+        "true_coverage_sampled_rows": cov,
         "sample": (f"oracle (float64 numpy, BLAS threads={cores}) plan+select of heads {hv} (VS) and "
                    f"{hq} (QA) of {w.name} plus sparse attention of {i} q-blocks per head "
                    f"({blocks} blocks); layer time extrapolated = H/2*(plan+select of both) + "
@@ -517,10 +537,18 @@ def main():
         r["fpl"].select(w.gamma, w.min_budget, with_stats=True)
     torch.cuda.synchronize()
     nnz, patterns = [], []
+    per_head = {"pattern": [], "jsd": [], "k_v": [], "k_s": [], "k_qa": [], "density": [],
+                "budget_added": []}
     for r in runs:
-        for s_ in r["fpl"].stats():
+        jsd = r["fpl"].jsd.cpu().tolist()
+        for i, s_ in enumerate(r["fpl"].stats()):
             nnz.append(s_["nnz_blocks"])
             patterns.append(s_["pattern"])
+            per_head["pattern"].append(int(s_["pattern"]))
+            per_head["jsd"].append(round(float(jsd[i]), 5))
+            for key in ("k_v", "k_s", "k_qa", "budget_added"):
+                per_head[key].append(int(s_[key]))
+            per_head["density"].append(round(s_["nnz_blocks"] / (nb * (nb + 1) / 2), 4))
     f_useful = useful_flops(nnz, nb)
     f_issued = sum(4 * 128 * 128 * 128 * x for x in nnz)
     density = float(np.sum(nnz)) / (len(nnz) * nb * (nb + 1) / 2)
@@ -578,7 +606,8 @@ def main():
     if rank == 0 and world == 1 and not a.no_cpu:
         o = oracle_sample(w, a.cpu_budget_s, nnz_per_head=nnz)
         cpu = {"value": n / o["est_layer_s"], "unit": "tokens/s", "cores": o["cores"],
-               "kind": "oracle", "sample": o["sample"], "est_layer_s": o["est_layer_s"]}
+               "kind": "oracle", "sample": o["sample"], "est_layer_s": o["est_layer_s"],
+               "true_coverage_sampled_rows": o["true_coverage_sampled_rows"]}
 
     if rank == 0:
         line = {
@@ -606,6 +635,7 @@ def main():
             "dense_tflops": (dense_flops(H, n) / (dense_ms / 1e3) / 1e12) if dense_ms else None,
             "density": density,
             "patterns": {"qa": int(np.sum(patterns)), "vs": int(len(patterns) - np.sum(patterns))},
+            "per_head": per_head,
             "roofline": {"bound": "tensor", "kernel": "fp_sparse_attn (attn8_kernel)",
                          "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
                          "frac": achieved / peak_sus, "frac_of_burst": achieved / peak_burst,
