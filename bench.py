@@ -269,7 +269,23 @@ def run_balanced(a, w, world, rank, local_rank):
     v = torch.from_numpy(vb_).view(torch.bfloat16).to(dev)
     del qb_, kb_, vb_
     exch = dict(exchange="nccl")
-    if a.exchange == "p2p":
+    share = os.environ.get("FP_BENCH_SHARE_GPU") == "1"
+    if a.exchange == "p2p" and share:
+        # validation on one GPU: ranks share the device, so symmetric memory is
+        # unavailable; map the other ranks' output buffers with CUDA IPC instead
+        # (same addressing / protocol as over NVLink), host barrier per step
+        from torch.multiprocessing.reductions import reduce_tensor
+        out = torch.zeros((H, n, 128), dtype=torch.bfloat16, device=dev)
+        handles = [None] * world
+        dist.all_gather_object(handles, reduce_tensor(out))
+        peer_views = [out if r == rank else handles[r][0](*handles[r][1]) for r in range(world)]
+
+        def host_barrier():
+            torch.cuda.synchronize()
+            dist.barrier()
+        exch = dict(exchange="p2p", peer_bases=[t.data_ptr() for t in peer_views],
+                    head_bytes=n * 128 * 2, barrier=host_barrier)
+    elif a.exchange == "p2p":
         # next row f4, fused exchange: the layer output is one symmetric-memory
         # allocation; every attention launch also stores its rows into the other
         # ranks' copies over NVLink (fp_sparse_attn_peers), one barrier per step
@@ -340,6 +356,21 @@ def run_balanced(a, w, world, rank, local_rank):
               "attn": span("t2", "t3"), "gather_exposed": span("t3", "t4")}
     assign, costs = layer.last_assignment, layer.last_costs
     f_mine = sum(costs[h] for h in assign[rank])
+    p2p_check = None
+    if True:
+        # every rank's buffer must hold the whole layer after the step: compare
+        # with this rank's own single-process computation of all heads (bitwise:
+        # same kernels, same inputs)
+        layer.step(out)
+        torch.cuda.synchronize()
+        ref_fpl = fp.FlexPrefill(H, G, n, device=dev)
+        ref = torch.empty_like(out)
+        ref_fpl.layer(q, k, v, ref, w.gamma, w.tau, w.min_budget)
+        torch.cuda.synchronize()
+        ok = torch.tensor([1 if torch.equal(ref, out) else 0],
+                          device="cpu" if dist.get_backend() == "gloo" else dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        p2p_check = bool(ok.item())  # both exchanges (broadcast rounds / fused peer stores)
     achieved = f_mine / (stages["attn"] / 1e3) / 1e12
 
     # dense baseline: static contiguous heads + all-gather (uniform cost per head)
@@ -392,6 +423,7 @@ def run_balanced(a, w, world, rank, local_rank):
                                if a.exchange == "p2p" else "overlapped output broadcasts"),
                            l2=l2_note(w)),
             "latency_ms_per_layer": ms_step, "stage_ms_rank0": stages,
+            "output_check": p2p_check,
             "dense_ms_per_layer": dense_ms,
             "speedup_vs_dense": (dense_ms / ms_step) if dense_ms else None,
             "imbalance": {"lpt": fpdist.imbalance(costs, assign), "static": static_imb},
@@ -426,11 +458,19 @@ def main():
     if world != a.gpus and not (world == 1 and a.gpus == 1):
         if rank == 0:
             print(f"warning: --gpus {a.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    # FP_BENCH_SHARE_GPU=1 (validation only, never a bench number): several ranks on
+    # one GPU with the gloo backend, to exercise the multi-rank code path on a 1-GPU box
+    share = os.environ.get("FP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     # torchrun (even with one rank) -> NCCL process group and the output all-gather
     dist_on = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
     if dist_on:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     fp.load_library()
     dev = torch.device("cuda", local_rank)
     H, G, n = w.heads, w.kv_heads, w.seq_len
