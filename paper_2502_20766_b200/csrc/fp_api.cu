@@ -280,9 +280,10 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
   if (ws_bytes < fp_workspace_bytes(heads, kv_heads, seq_len, head_dim, block_size))
     return FP_ERR_WORKSPACE;
   if ((st = check_device())) return st;
-  // Pipelined per KV group (g = heads / kv_heads Q heads + their K/V): host->
-  // device copies of group c+1 and the device->host copy of group c-1 overlap
-  // the compute of group c (three streams joined back to `stream`). Groups use
+  // Pipelined per chunk of Q heads (a KV group, g = heads / kv_heads Q heads +
+  // their K/V; the first group split into single heads): host->device copies of
+  // chunk c+1 and the device->host copies of chunk c-1 overlap the compute of
+  // chunk c (three streams joined back to `stream`). Chunks alternate between
   // two workspace slots (the full-layer workspace holds at least two).
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   const int g = heads / kv_heads;
@@ -308,47 +309,58 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
     chk(cudaStreamWaitEvent(scomp, e_start, 0));
     chk(cudaStreamWaitEvent(sout, e_start, 0));
   }
-  for (int c = 0; c < kv_heads && e == cudaSuccess && st == FP_OK; ++c) {
-    const char* qh = static_cast<const char*>(q_host) + c * qb_bytes;
+  // Chunks of Q heads: the first KV group one head at a time (only its K + one
+  // head of Q is uploaded before compute starts), every later group whole.
+  struct Chunk {
+    int grp, h0, nh;
+  };
+  const size_t hb = qb_bytes / g;  // one head of Q / O
+  int nchunk = 0;
+  for (int c = 0; c < kv_heads; ++c) nchunk += (c == 0) ? g : 1;
+  for (int ci_ = 0; ci_ < nchunk && e == cudaSuccess && st == FP_OK; ++ci_) {
+    const Chunk ch = ci_ < g ? Chunk{0, ci_, 1} : Chunk{ci_ - g + 1, 0, g};
+    const int c = ch.grp;
+    const bool first_of_group = (ch.h0 == 0);
+    const char* qh = static_cast<const char*>(q_host) + c * qb_bytes + ch.h0 * hb;
     const char* kh = static_cast<const char*>(k_host) + c * kv_bytes;
     const char* vh = static_cast<const char*>(v_host) + c * kv_bytes;
-    char* qd = static_cast<char*>(d_q) + c * qb_bytes;
+    char* qd = static_cast<char*>(d_q) + c * qb_bytes + ch.h0 * hb;
     char* kd = static_cast<char*>(d_k) + c * kv_bytes;
     char* vd = static_cast<char*>(d_v) + c * kv_bytes;
-    char* od = static_cast<char*>(d_o) + c * qb_bytes;
+    char* od = static_cast<char*>(d_o) + c * qb_bytes + ch.h0 * hb;
     // K and Q first (all fp_plan / fp_select read), V last (only the attention
-    // reads it); the attention runs one launch per head (bitwise the same
-    // result: work items are per (head, query block)) and each head's output
-    // is copied back as soon as it is done, so only the last head's D2H is
-    // exposed at the end.
+    // reads it); K / V once per group (with the group's first chunk). The
+    // attention runs one launch per head (bitwise the same result: work items
+    // are per (head, query block)) and each head's output is copied back as
+    // soon as it is done, so only the last head's D2H is exposed at the end.
     cudaEvent_t e_kq = nullptr, e_v = nullptr;
     chk(cudaEventCreateWithFlags(&e_kq, cudaEventDisableTiming));
     chk(cudaEventCreateWithFlags(&e_v, cudaEventDisableTiming));
-    chk(cudaMemcpyAsync(kd, kh, kv_bytes, cudaMemcpyHostToDevice, sin));
-    chk(cudaMemcpyAsync(qd, qh, qb_bytes, cudaMemcpyHostToDevice, sin));
+    if (first_of_group) chk(cudaMemcpyAsync(kd, kh, kv_bytes, cudaMemcpyHostToDevice, sin));
+    chk(cudaMemcpyAsync(qd, qh, ch.nh * hb, cudaMemcpyHostToDevice, sin));
     chk(cudaEventRecord(e_kq, sin));
-    chk(cudaMemcpyAsync(vd, vh, kv_bytes, cudaMemcpyHostToDevice, sin));
+    if (first_of_group) chk(cudaMemcpyAsync(vd, vh, kv_bytes, cudaMemcpyHostToDevice, sin));
     chk(cudaEventRecord(e_v, sin));
     chk(cudaStreamWaitEvent(scomp, e_kq, 0));
-    void* wsc = static_cast<char*>(ws) + (c % nslots) * slot;
-    int32_t* rp = row_ptr + (size_t)c * g * (nb + 1);
-    int32_t* ci = col_idx + (size_t)c * g * cap;
+    void* wsc = static_cast<char*>(ws) + (ci_ % nslots) * slot;
+    const int hg = c * g + ch.h0;  // first global head of the chunk
+    int32_t* rp = row_ptr + (size_t)hg * (nb + 1);
+    int32_t* ci = col_idx + (size_t)hg * cap;
     if (e == cudaSuccess &&
-        !(st = fp_plan(qd, kd, g, 1, seq_len, head_dim, block_size, tau, wsc, slot, pattern + c * g,
-                       jsd + c * g, scomp)))
-      st = fp_select(g, 1, seq_len, head_dim, block_size, gamma, min_budget, wsc, slot, rp, ci,
+        !(st = fp_plan(qd, kd, ch.nh, 1, seq_len, head_dim, block_size, tau, wsc, slot, pattern + hg,
+                       jsd + hg, scomp)))
+      st = fp_select(ch.nh, 1, seq_len, head_dim, block_size, gamma, min_budget, wsc, slot, rp, ci,
                      nullptr, scomp);
     chk(cudaStreamWaitEvent(scomp, e_v, 0));
-    const size_t hb = qb_bytes / g;  // one head of Q / O
-    for (int i = 0; i < g && e == cudaSuccess && st == FP_OK; ++i) {
+    for (int i = 0; i < ch.nh && e == cudaSuccess && st == FP_OK; ++i) {
       st = fp_sparse_attn(qd + i * hb, kd, vd, od + i * hb, 1, 1, seq_len, head_dim, block_size,
                           rp + (size_t)i * (nb + 1), ci + (size_t)i * cap, wsc, slot, scomp);
       cudaEvent_t e_h = nullptr;
       chk(cudaEventCreateWithFlags(&e_h, cudaEventDisableTiming));
       chk(cudaEventRecord(e_h, scomp));
       chk(cudaStreamWaitEvent(sout, e_h, 0));
-      chk(cudaMemcpyAsync(static_cast<char*>(o_host) + c * qb_bytes + i * hb, od + i * hb, hb,
-                          cudaMemcpyDeviceToHost, sout));
+      chk(cudaMemcpyAsync(static_cast<char*>(o_host) + c * qb_bytes + (ch.h0 + i) * hb, od + i * hb,
+                          hb, cudaMemcpyDeviceToHost, sout));
       if (e_h) cudaEventDestroy(e_h);
     }
     if (e_kq) cudaEventDestroy(e_kq);
