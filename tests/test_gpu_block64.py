@@ -121,3 +121,40 @@ def test_block64_glm_group16_stagewise(fp):
     _check_plan(w, res, _oracle_plans(w, Q, K, heads=[0, 1, 15, 16, 31], b=B))
     _check_select_stagewise(w, res, w.gamma, w.min_budget, B)
     _check_attn_stagewise(w, res, Q, K, V, qblocks=[0, 1, 7, 15, 16, 31], b=B)
+
+
+def test_block64_layer_host_matches_device_path(fp):
+    """the host-buffer pipeline (fp_layer_host) at b = 64 gives the device path's
+    CSR and outputs bitwise."""
+    import torch
+    w = Workload("b64-host", 8, 2, 2085, 0.9, 0.1, 512, 141)
+    q, k, v = gen.make_layer_bits(w)
+    res = parity.run_gpu(fp, w, q, k, v, block_size=B)
+    fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len, block_size=B)
+    qh, kh, vh = (torch.from_numpy(x).view(torch.bfloat16).pin_memory() for x in (q, k, v))
+    oh = torch.empty_like(qh).pin_memory()
+    dq, dk, dv = (torch.empty(x.shape, dtype=torch.bfloat16, device="cuda") for x in (qh, kh, vh))
+    do = torch.empty_like(dq)
+    fp.fp_layer_host(qh, kh, vh, oh, dq, dk, dv, do, w.heads, w.kv_heads, w.seq_len, w.gamma, w.tau,
+                     w.min_budget, fpl.ws, fpl.ws_bytes, fpl.pattern, fpl.jsd, fpl.row_ptr,
+                     fpl.col_idx, block_size=B)
+    torch.cuda.synchronize()
+    assert np.array_equal(fpl.row_ptr.cpu().numpy(), res["row_ptr"])
+    assert np.array_equal(oh.float().numpy(), res["out"])
+
+
+def test_block64_peers_not_supported(fp):
+    """the fused output exchange is implemented by the b = 128 kernel only: the
+    b = 64 call fails loudly (FP_ERR_CUDA / cudaErrorNotSupported), nothing silent."""
+    import torch
+    w = Workload("b64-peers", 4, 1, 1024, 0.9, 0.1, 0, 143)
+    q, k, v = (parity.to_torch_bf16(x) for x in gen.make_layer_bits(w))
+    fpl = fp.FlexPrefill(4, 1, 1024, block_size=B)
+    fpl.plan(q, k, 0.1)
+    fpl.select(0.9, 0)
+    out = torch.zeros_like(q)
+    peer = torch.zeros_like(q)
+    ptrs = torch.tensor([peer.data_ptr()], dtype=torch.int64, device="cuda")
+    with pytest.raises(fp.FlexPrefillError):
+        fp.fp_sparse_attn_peers(q, k, v, out, ptrs, 1, 4, 1, 1024, fpl.row_ptr, fpl.col_idx,
+                                block_size=B)
