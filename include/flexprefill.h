@@ -23,8 +23,10 @@
  *  - seq_len is any n >= 128; nb = ceil(n / 128) blocks, the last one ragged
  *    when n % 128 != 0 (reading A26).
  *  - Every tensor / workspace pointer is a DEVICE pointer unless the name
- *    says host. The caller owns all memory; the library never allocates, keeps
- *    no per-call state, and only enqueues work on `stream` (no host syncs), so
+ *    says host. The caller owns all memory; the library never allocates device
+ *    memory, keeps no per-call state, and only enqueues work ordered on `stream`
+ *    (no host syncs; fp_plan at short lengths forks one branch onto an internal
+ *    per-device side stream and joins it back through events before returning), so
  *    fp_plan -> fp_select -> fp_sparse_attn is CUDA-graph capturable. Stages
  *    communicate through the workspace; data-dependent sizes stay on device.
  *  - Validation is synchronous and happens before anything is enqueued; an

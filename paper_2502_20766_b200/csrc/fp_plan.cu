@@ -18,6 +18,8 @@
 //   pooled_softmax N4c A_bar row softmax over kb <= qb, / nb (QA heads only)
 #include <math.h>
 
+#include <mutex>
+
 #include "fp_common.cuh"
 #include "fp_internal.h"
 
@@ -422,7 +424,7 @@ __global__ void qbar_kernel(const __nv_bfloat16* __restrict__ q, TLayout ql,
                             const int32_t* __restrict__ pattern, int n, int nb, int b,
                             float* __restrict__ q_bar) {
   const int qb = blockIdx.x, h = blockIdx.y;
-  if (pattern[h] != 1) return;
+  if (pattern && pattern[h] != 1) return;  // pattern == nullptr: every head
   const uint16_t* qh = reinterpret_cast<const uint16_t*>(q) + toff(ql, h, qb * b) + threadIdx.x;
   const int cnt = min(b, n - qb * b);
   float acc = 0.f;
@@ -442,7 +444,7 @@ __global__ void __launch_bounds__(256) pooled_logits(
     const int32_t* __restrict__ pattern, int H, int G, int nb, float scale,
     float* __restrict__ A_bar) {
   const int rt = blockIdx.x, ct = blockIdx.y, h = blockIdx.z;
-  if (ct > rt || pattern[h] != 1) return;
+  if (ct > rt || (pattern && pattern[h] != 1)) return;
   __shared__ float qs[kPT][129];
   __shared__ float ks[kPT][129];
   const int g = h / (H / G);
@@ -477,7 +479,7 @@ __global__ void __launch_bounds__(kMapThreads) pooled_softmax(const int32_t* __r
                                                               int nb, float* __restrict__ A_bar) {
   __shared__ float red[33];
   const int qb = blockIdx.x, h = blockIdx.y;
-  if (pattern[h] != 1) return;
+  if (pattern && pattern[h] != 1) return;
   float* row = A_bar + (size_t)h * ((size_t)nb * (nb + 1) / 2) + (size_t)qb * (qb + 1) / 2;
   const int tid = threadIdx.x;
   float mx = -INFINITY;
@@ -491,6 +493,22 @@ __global__ void __launch_bounds__(kMapThreads) pooled_softmax(const int32_t* __r
 }
 
 }  // namespace
+
+// One non-blocking side stream per device for the pooled-map branch of fp_plan,
+// created on first use (the library's only lazily initialised state besides
+// kernel attributes). nullptr if it cannot be created: the branch then runs
+// in order on the caller's stream.
+cudaStream_t plan_side_stream() {
+  static cudaStream_t streams[64] = {};
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::call_once(once[dev], [&]() {
+    if (cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
+      streams[dev] = nullptr;
+  });
+  return streams[dev];
+}
 
 size_t rep_smem_bytes(int pass) {
   size_t b = sizeof(RepSmem);
@@ -517,10 +535,50 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
   dim3 grid(s.nchunks, s.H);
   (void)k;
   const int Hp = lay.q.per, Gp = lay.k.per;
+  // The Query-Aware pooled map (a3: q_bar, pooled logits, row softmax) needs
+  // only Q and K_bar, not the pattern: it can run for EVERY head on a side stream,
+  // concurrently with rep_stats .. pattern_kernel, and is joined back before
+  // fp_plan returns (VS heads' maps are computed and ignored). This takes the
+  // three kernels off the stage's critical path (they are latency-bound at
+  // short n). Fork / join through events: stream-ordered and graph-capturable.
+  // Only for short sequences (nb <= 256 blocks): there the three kernels are
+  // latency-bound and the extra maps of the VS heads are cheap; at 128k the
+  // all-heads map costs more than it hides (measured with tools/plan_ab.py:
+  // 4k plan 0.100 -> 0.083 ms, 8k 0.132 -> 0.117, 32k equal, 128k 1.42 -> 1.87).
+  cudaStream_t side = s.nb <= 256 ? plan_side_stream() : nullptr;
+  cudaEvent_t e_fork = nullptr, e_kbar = nullptr, e_join = nullptr;
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t r) {
+    if (e == cudaSuccess && r != cudaSuccess) e = r;
+  };
+  if (side) {
+    chk(cudaEventCreateWithFlags(&e_fork, cudaEventDisableTiming));
+    chk(cudaEventCreateWithFlags(&e_kbar, cudaEventDisableTiming));
+    chk(cudaEventCreateWithFlags(&e_join, cudaEventDisableTiming));
+    chk(cudaEventRecord(e_fork, st));
+    chk(cudaStreamWaitEvent(side, e_fork, 0));
+  }
+  const int32_t* qa_only = side ? nullptr : wsp<int32_t>(ws, L.pattern);
+  cudaStream_t sq = side ? side : st;
+  const int nt = (s.nb + kPT - 1) / kPT;
+  auto pooled_map = [&]() {
+    qbar_kernel<<<dim3(s.nb, s.H), 128, 0, sq>>>(reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
+                                                 qa_only, s.n, s.nb, s.b, wsp<float>(ws, L.q_bar));
+    if (side) chk(cudaStreamWaitEvent(side, e_kbar, 0));  // K_bar from rep_pass<1>
+    pooled_logits<<<dim3(nt, nt, s.H), 256, 0, sq>>>(wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar),
+                                                     qa_only, s.H, s.G, s.nb, scale,
+                                                     wsp<float>(ws, L.A_bar));
+    pooled_softmax<<<dim3(s.nb, s.H), kMapThreads, 0, sq>>>(qa_only, s.nb, wsp<float>(ws, L.A_bar));
+  };
   rep_pass<1><<<grid, kRepThreads, sm1, st>>>(qmap, kmap, s.H, s.G, Hp, Gp, s.n, s.nb, s.nt, s.b, s.nchunks, s.ct, scale_log2,
                                               m_part, l_part, m_row, il_row,
                                               wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_v),
                                               wsp<float>(ws, L.as_part));
+  if (side) {
+    chk(cudaEventRecord(e_kbar, st));
+    pooled_map();
+    chk(cudaEventRecord(e_join, side));
+  }
   rep_stats<<<s.H, 128, 0, st>>>(s.nchunks, m_part, l_part, m_row, il_row);
   rep_pass<2><<<grid, kRepThreads, sm2, st>>>(qmap, kmap, s.H, s.G, Hp, Gp, s.n, s.nb, s.nt, s.b, s.nchunks, s.ct, scale_log2,
                                               m_part, l_part, m_row, il_row,
@@ -537,15 +595,15 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
       reinterpret_cast<const __nv_bfloat16*>(q), lay.q, wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_hat),
       s.H, s.G, s.n, s.nb, s.b, scale, tau, wsp<float>(ws, L.a_bar), wsp<int32_t>(ws, L.pattern),
       wsp<float>(ws, L.jsd), pattern_out, jsd_out);
-  qbar_kernel<<<dim3(s.nb, s.H), 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
-                                               wsp<int32_t>(ws, L.pattern), s.n, s.nb, s.b,
-                                               wsp<float>(ws, L.q_bar));
-  const int nt = (s.nb + kPT - 1) / kPT;
-  pooled_logits<<<dim3(nt, nt, s.H), 256, 0, st>>>(wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar),
-                                                   wsp<int32_t>(ws, L.pattern), s.H, s.G, s.nb,
-                                                   scale, wsp<float>(ws, L.A_bar));
-  pooled_softmax<<<dim3(s.nb, s.H), kMapThreads, 0, st>>>(wsp<int32_t>(ws, L.pattern), s.nb,
-                                                          wsp<float>(ws, L.A_bar));
+  if (side) {
+    chk(cudaStreamWaitEvent(st, e_join, 0));
+  } else {
+    pooled_map();  // no side stream: QA heads only, after the pattern
+  }
+  if (e_fork) cudaEventDestroy(e_fork);
+  if (e_kbar) cudaEventDestroy(e_kbar);
+  if (e_join) cudaEventDestroy(e_join);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
