@@ -668,6 +668,7 @@ def main():
                            l2=l2_note(w)),
             "latency_ms_per_layer": ms_step,
             "ms_per_step_cuda_graph": graph_ms,
+            "ms_per_step_median": float(np.median(ms_list)), "ms_per_step_min": float(np.min(ms_list)),
             "stage_ms": {"plan": plan_ms, "select": sel_ms, "attn": attn_ms},
             "dense_ms_per_layer": dense_ms,
             "speedup_vs_dense": (dense_ms / ms_step) if dense_ms else None,
