@@ -41,6 +41,19 @@
 #include "fp_common.cuh"
 #include "fp_internal.h"
 
+#ifdef FP_TIMING
+// clock64 phase accumulators (tools/attn8_timing.py): [0..5] softmax thread 0
+// of each row, [8..12] the MMA issuer, [14] issuer entries, [15] softmax tiles
+__device__ unsigned long long g_attn8_timing[16];
+#define FP_T8(k) do { if (t_on) { long long _t = clock64(); tacc[k] += _t - tlast; tlast = _t; } } while (0)
+#define FP_T8_DECL(on) const bool t_on = (on); long long tacc[16] = {0}; long long tlast = clock64()
+#define FP_T8_FLUSH(lo, hi) do { if (t_on) for (int _k = lo; _k < hi; ++_k) atomicAdd(&g_attn8_timing[_k], (unsigned long long)tacc[_k]); } while (0)
+#else
+#define FP_T8(k) do { } while (0)
+#define FP_T8_DECL(on) do { } while (0)
+#define FP_T8_FLUSH(lo, hi) do { } while (0)
+#endif
+
 namespace fp {
 
 namespace {
@@ -58,6 +71,20 @@ constexpr float kRescale8 = 8.0f;  // lazy rescale: tolerate P up to 2^8 (as v5)
 #define FP_EMU8 0
 #endif
 constexpr int kEmu8 = FP_EMU8;
+// P handed to the tensor core in two halves (keys 0-63, 64-127): the softmax
+// stores P in 32-key chunks as the exponentials finish (tcgen05.st overlaps
+// the next chunk's MUFU work) and arrives on p_lo after the first half, so
+// the issuer starts PV's first four k-steps while the second half is still
+// being exponentiated. Bitwise equal to the unsplit path; measured (C3,
+// alternating 12-launch blocks) 34.04-34.19 ms vs 34.20-34.79 ms sparse, equal
+// dense (profiles/r01_v8_phase_timing.txt). The gain is small because a row's
+// period is bound by its single S buffer (S(e+1) waits for softmax(e) and
+// PV(e)): the MMA pipeline alone runs at 3147 cycles per union entry against
+// 2048 of tensor work (the -DFP_XSM8 experiment), see DESIGN.md section 6.
+#ifndef FP_SPLIT8
+#define FP_SPLIT8 1
+#endif
+constexpr bool kSplit8 = FP_SPLIT8 != 0;
 
 struct Attn8Smem {
   uint8_t q[2][kTileBytes];  // Q_A, Q_B (1024-B aligned: first member)
@@ -66,7 +93,7 @@ struct Attn8Smem {
   uint64_t q_full;
   uint64_t k_full[kKS8], k_empty[kKS8];
   uint64_t v_full[kVS8], v_empty[kVS8];
-  uint64_t s_full[2], p_full[2], pv_done[2];
+  uint64_t s_full[2], p_full[2], p_lo[2], pv_done[2];
   uint32_t tmem_base;
 };
 
@@ -162,6 +189,18 @@ FP_DEV void umma_pv_chain8(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc,
       "l"(b0 + 640), "l"(b0 + 768), "l"(b0 + 896), "r"(idesc), "r"(acc0));
 }
 
+// Half of O += P V: 4 k-steps (64 keys) starting at P column a0 / V descriptor b0.
+FP_DEV void umma_pv_chain4(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %9, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %6, %9, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %7, %9, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %8, %9, p;\n\t}" ::"r"(d),
+      "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "l"(b0), "l"(b0 + 128), "l"(b0 + 256),
+      "l"(b0 + 384), "r"(idesc), "r"(acc0));
+}
+
 // Merge of the two rows' sorted key-block lists: next union entry.
 // mask bit 0: row A selected it, bit 1: row B.
 struct UnionIter {
@@ -240,6 +279,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
     for (int x = 0; x < 2; ++x) {
       mbar_init(&sm.s_full[x], 1);
       mbar_init(&sm.p_full[x], 4);  // one arrival per softmax warp of the stream
+      mbar_init(&sm.p_lo[x], 4);
       mbar_init(&sm.pv_done[x], 1);
     }
     mbar_fence_init();
@@ -287,14 +327,36 @@ __global__ void __launch_bounds__(kThreads8, 1)
         const uint64_t qdesc[2] = {sdesc_kmajor(smem_u32(sm.q[0]), 0), sdesc_kmajor(smem_u32(sm.q[1]), 0)};
         int pend[2] = {-1, -1};  // union entry of X's S awaiting its PV
         int cnt[2] = {0, 0};     // S tiles issued per stream
+        FP_T8_DECL(true);
         auto issue_pv = [&](int x) {
           const int e = pend[x];
           const int vs = e % kVS8;
+          FP_T8(12);
           mbar_wait(&sm.v_full[vs], (e / kVS8) & 1);
-          mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
-          tc_fence_after();
-          umma_pv_chain8(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128,
-                         sdesc_mnmajor(smem_u32(sm.v[vs]), 0), idesc_o, cnt[x] > 1);
+          FP_T8(9);
+          const uint64_t vdesc = sdesc_mnmajor(smem_u32(sm.v[vs]), 0);
+          if (kSplit8) {
+            mbar_wait(&sm.p_lo[x], (cnt[x] - 1) & 1);
+            FP_T8(10);
+            tc_fence_after();
+#if !defined(FP_XMMA8) && !defined(FP_XPV8)
+            umma_pv_chain4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
+                           cnt[x] > 1);
+#endif
+            FP_T8(12);
+            mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
+            FP_T8(11);
+            tc_fence_after();
+#if !defined(FP_XMMA8) && !defined(FP_XPV8)
+            umma_pv_chain4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512,
+                           idesc_o, 1);
+#endif
+          } else {
+            mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
+            tc_fence_after();
+            umma_pv_chain8(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
+                           cnt[x] > 1);
+          }
           umma_commit(&sm.v_empty[vs]);
           umma_commit(&sm.pv_done[x]);
           pend[x] = -1;
@@ -305,14 +367,21 @@ __global__ void __launch_bounds__(kThreads8, 1)
           int mask;
           it.next(mask);
           const int ks = e % kKS8;
+          FP_T8(12);
           mbar_wait(&sm.k_full[ks], (e / kKS8) & 1);
+          FP_T8(8);
+#ifdef FP_TIMING
+          ++tacc[14];
+#endif
           tc_fence_after();
           const uint64_t kdesc = sdesc_kmajor(smem_u32(sm.k[ks]), 0);
 #pragma unroll
           for (int x = 0; x < 2; ++x) {
             if (pend[x] >= 0) issue_pv(x);
             if (mask & (1 << x)) {
+#if !defined(FP_XMMA8) && !defined(FP_XS8)
               umma_ss_chain8(tbase + kColS8 + x * 128, qdesc[x], kdesc, idesc_s);
+#endif
               umma_commit(&sm.s_full[x]);
               pend[x] = e;
               ++cnt[x];
@@ -325,6 +394,8 @@ __global__ void __launch_bounds__(kThreads8, 1)
         }
         if (pend[0] >= 0) issue_pv(0);
         if (pend[1] >= 0) issue_pv(1);
+        FP_T8(12);
+        FP_T8_FLUSH(8, 15);
       }
     }
   } else {
@@ -338,36 +409,115 @@ __global__ void __launch_bounds__(kThreads8, 1)
     const uint32_t tS = tbase + kColS8 + x * 128 + lane_off;
     const uint32_t tO = tbase + kColO8 + x * 128 + lane_off;
     float m_used = -INFINITY, l = 0.f;
+    FP_T8_DECL((wid & 3) == 0 && lane_id() == 0);
     for (int t = 0; t < nX; ++t) {
+      FP_T8(6);
       mbar_wait(&sm.s_full[x], t & 1);
+      FP_T8(0);
+#ifdef FP_XSM8
+      // experiment: softmax does no work (measures the MMA/issuer pipeline alone)
+      tc_fence_after();
+      __syncwarp();
+      if (lane_id() == 0) { mbar_arrive(&sm.p_lo[x]); mbar_arrive(&sm.p_full[x]); }
+      continue;
+#endif
       tc_fence_after();
       float v[128];
       tmem_ld_32x32b_x64_8(tS, reinterpret_cast<uint32_t*>(v));
       tmem_ld_32x32b_x64_8(tS + 64, reinterpret_cast<uint32_t*>(v + 64));
       tmem_wait_ld();
+      FP_T8(1);
       if (t == nX - 1) {  // the diagonal block: keys j <= r only
 #pragma unroll
         for (int c = 0; c < 128; ++c)
           if (c > r) v[c] = -INFINITY;
       }
-      float m0 = fmax3_8(v[0], v[1], v[2]), m1 = fmax3_8(v[3], v[4], v[5]);
-      float m2 = fmax3_8(v[6], v[7], v[8]), m3 = fmax3_8(v[9], v[10], v[11]);
+      // row max: 8 independent fmax3 chains (8 x 16 columns), then a tree
+      float mc[8];
 #pragma unroll
-      for (int c = 12; c < 124; c += 8) {
-        m0 = fmax3_8(m0, v[c], v[c + 1]);
-        m1 = fmax3_8(m1, v[c + 2], v[c + 3]);
-        m2 = fmax3_8(m2, v[c + 4], v[c + 5]);
-        m3 = fmax3_8(m3, v[c + 6], v[c + 7]);
-      }
-      m0 = fmax3_8(m0, v[124], v[125]);
-      m1 = fmax3_8(m1, v[126], v[127]);
-      const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * scale_log2;
+      for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(v[16 * j], v[16 * j + 1], v[16 * j + 2]);
+#pragma unroll
+      for (int c = 3; c < 15; c += 2)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(mc[j], v[16 * j + c], v[16 * j + c + 1]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mc[j] = fmaxf(mc[j], v[16 * j + 15]);
+      const float mx = fmaxf(fmax3_8(mc[0], mc[1], mc[2]), fmax3_8(mc[3], mc[4], fmax3_8(mc[5], mc[6], mc[7]))) *
+                       scale_log2;
       float alpha = 1.f;
       if (mx > m_used + kRescale8) {
         alpha = exp2f(m_used - mx);  // 0 on the first tile
         m_used = mx;
       }
       const float nm = -m_used;
+      FP_T8(2);
+      if (kSplit8) {
+        // O_X holds sum_{earlier} P V: PV of the previous tile completed before
+        // S of this one (one in-order tcgen05.mma stream), so O can be
+        // rescaled now, before PV's first half is released
+        // (pv_done is waited for only when O is touched: the barrier cannot run
+        // ahead of this thread, PV(t) needs this tile's P)
+        if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          mbar_wait(&sm.pv_done[x], (t - 1) & 1);
+          {
+            tc_fence_after();
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint32_t ov[32];
+              tmem_ld32(tO + q4 * 32, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
+              tmem_st32(tO + q4 * 32, ov);
+            }
+          }
+        }
+        FP_T8(3);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          const int c0 = ch * 32;
+#pragma unroll
+          for (int c = c0; c < c0 + 32; c += 2) ffma2_8(v[c], v[c + 1], v[c], v[c + 1], scale_log2, nm);
+#pragma unroll
+          for (int c = c0; c < c0 + 32; ++c)
+            if (c < 128 - kEmu8) v[c] = fast_exp2(v[c]);
+#pragma unroll
+          for (int c = c0; c < c0 + 32; c += 2)
+            if (c >= 128 - kEmu8) exp2_emu2_8(v[c], v[c + 1], v[c], v[c + 1]);
+          if (kEmu8 > 0 && t == nX - 1) {
+#pragma unroll
+            for (int c = c0; c < c0 + 32; ++c)
+              if (c >= 128 - kEmu8 && c > r) v[c] = 0.f;
+          }
+#pragma unroll
+          for (int c = c0; c < c0 + 32; c += 4) {
+            fadd2_8(s0, s1, s0, s1, v[c], v[c + 1]);
+            fadd2_8(s2, s3, s2, s3, v[c + 2], v[c + 3]);
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk[c] = pack_bf16x2(v[c0 + 2 * c], v[c0 + 2 * c + 1]);
+          tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
+          if (ch == 1) {
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&sm.p_lo[x]);
+            FP_T8(4);
+          }
+        }
+        l = l * alpha + ((s0 + s1) + (s2 + s3));
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&sm.p_full[x]);
+        FP_T8(5);
+#ifdef FP_TIMING
+        ++tacc[15];
+#endif
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < 128; c += 2) ffma2_8(v[c], v[c + 1], v[c], v[c + 1], scale_log2, nm);
 #pragma unroll
@@ -411,6 +561,10 @@ __global__ void __launch_bounds__(kThreads8, 1)
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&sm.p_full[x]);
     }
+    FP_T8_FLUSH(0, 8);
+#ifdef FP_TIMING
+    if (t_on) atomicAdd(&g_attn8_timing[15], (unsigned long long)tacc[15]);
+#endif
     if (nX > 0) {
       // epilogue: O / l -> bf16 -> global (rows past n are not stored)
       mbar_wait(&sm.pv_done[x], (nX - 1) & 1);
@@ -454,6 +608,17 @@ __global__ void __launch_bounds__(kThreads8, 1)
 }  // namespace
 
 size_t attn8_smem_bytes() { return sizeof(Attn8Smem); }
+
+#ifdef FP_TIMING
+extern "C" int fp_debug_attn8_timing(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_attn8_timing, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_attn8_timing, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
