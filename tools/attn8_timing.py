@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("lib")
 ap.add_argument("--workload", default="C3-llama8b-128k")
 ap.add_argument("--dense", action="store_true")
+ap.add_argument("--v11", action="store_true")
 a = ap.parse_args()
 fp.load_library(os.path.abspath(a.lib))
 import torch  # noqa: E402
@@ -33,25 +34,26 @@ fpl.select(w.gamma, w.min_budget)
 run = (lambda: fpl.dense(q, k, v, out)) if a.dense else (lambda: fpl.attn(q, k, v, out))
 raw = ctypes.CDLL(os.path.abspath(a.lib))
 buf = (ctypes.c_ulonglong * 16)()
+dbg = raw.fp_debug_attn11_timing if a.v11 else raw.fp_debug_attn8_timing
 run()
 torch.cuda.synchronize()
-raw.fp_debug_attn8_timing(buf, 1)
+dbg(buf, 1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 run()
 e1.record()
 torch.cuda.synchronize()
-raw.fp_debug_attn8_timing(buf, 1)
+dbg(buf, 1)
 tiles, ents = max(buf[15], 1), max(buf[14], 1)
 print(f"{w.name} {'dense' if a.dense else 'sparse'}: {e0.elapsed_time(e1):.3f} ms, softmax tiles "
       f"(thread 0 of each row) {tiles}, issuer entries {ents}")
-names = {0: "wait S", 1: "S ld", 2: "max/alpha", 3: "O rescale", 4: "P lo (exp+st)",
+names = {0: "wait S", 1: "softmax", 2: "P wait st", 3: "arrive"} if a.v11 else {0: "wait S", 1: "S ld", 2: "max/alpha", 3: "O rescale", 4: "P lo (exp+st)",
          5: "P hi (exp+st)", 6: "loop"}
 tot = sum(buf[i] for i in names)
 for i, nm in names.items():
     print(f"  softmax {nm:16s} {buf[i] / tiles:8.1f} cyc/tile  {100 * buf[i] / max(tot, 1):5.1f}%")
 print(f"  softmax total            {tot / tiles:8.1f} cyc/tile")
-inames = {8: "wait K", 9: "wait V", 10: "wait P lo", 11: "wait P hi", 12: "issue/other"}
+inames = {8: "wait K", 9: "wait V", 10: "wait P lo" if not a.v11 else "wait P WG0", 11: "wait P hi" if not a.v11 else "wait P WG1", 12: "issue/other"}
 itot = sum(buf[i] for i in inames)
 for i, nm in inames.items():
     print(f"  issuer  {nm:16s} {buf[i] / ents:8.1f} cyc/entry  {100 * buf[i] / max(itot, 1):5.1f}%")
