@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-vendor", action="store_true",
+                    help="skip the vendor dense context (torch SDPA, cuDNN backend)")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
                     help="N > 1 with --balance lpt: output exchange by NCCL broadcast rounds, or "
@@ -605,6 +607,27 @@ def main():
     dense_ms = None
     if not a.no_dense:
         dense_ms, _ = timed(dense_step, max(2, min(a.steps, 5)), 1)
+    # ---- context: the vendor dense causal kernel on the same GPU (torch SDPA,
+    # cuDNN backend; GQA by repeating K/V heads). Not on the product path.
+    vendor = None
+    if not a.no_dense and not a.no_vendor and len(runs) == 1 and not dist_on:
+        try:
+            from torch.nn.attention import SDPBackend, sdpa_kernel
+            r0 = runs[0]
+            rep = r0["q"].shape[0] // r0["k"].shape[0]
+            kr = r0["k"].repeat_interleave(rep, 0).unsqueeze(0)
+            vr = r0["v"].repeat_interleave(rep, 0).unsqueeze(0)
+            q4 = r0["q"].unsqueeze(0)
+
+            def vendor_step():
+                with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+                    torch.nn.functional.scaled_dot_product_attention(q4, kr, vr, is_causal=True)
+            v_ms, _ = timed(vendor_step, max(2, min(a.steps, 5)), 1)
+            vendor = {"impl": "torch SDPA, cuDNN backend (dense causal, K/V heads repeated)",
+                      "ms_per_layer": v_ms, "tflops": dense_flops(H, n) / (v_ms / 1e3) / 1e12}
+            del kr, vr
+        except Exception as ex:  # backend unavailable
+            vendor = {"unavailable": str(ex).split("\n")[0][:200]}
     clk.__exit__(None, None, None)
     clocks = clk.summary()
 
@@ -674,6 +697,8 @@ def main():
             "speedup_vs_dense": (dense_ms / ms_step) if dense_ms else None,
             "attn_speedup_vs_dense": (dense_ms / attn_ms) if dense_ms else None,
             "dense_tflops": (dense_flops(H, n) / (dense_ms / 1e3) / 1e12) if dense_ms else None,
+            "dense_vendor": vendor,
+            "speedup_vs_vendor_dense": (vendor["ms_per_layer"] / ms_step) if vendor and "ms_per_layer" in vendor else None,
             "density": density,
             "patterns": {"qa": int(np.sum(patterns)), "vs": int(len(patterns) - np.sum(patterns))},
             "per_head": per_head,
