@@ -1,21 +1,25 @@
-// EXPERIMENT (round 1), NOT BUILT: the CTA-pair (cta_group::2) attention
-// kernel described below, kept as the starting point for the next round.
+// EXPERIMENT (round 1), NOT BUILT: a CTA-pair (cta_group::2, M = 256)
+// attention kernel, kept as the starting point for the next round.
 // Status, measured on B200 (profiles/r01_v11_experiment.txt):
-//   * runs and matches v8 on C1 (2k); at 32k rows 112-127 of the second CTA's
-//     query block (rank 1) disagree with v8 by up to 2.8 (dense) -- an
-//     unresolved ordering bug between that CTA's P stores and the leader's
-//     PV MMA, or in the rank-1 half loads;
-//   * 7.16 ms vs v8's 6.40 ms dense at 32k: with two S buffers shared by the
-//     two column-half warpgroups, S(e+1) can only be issued after PV(e-1), so
-//     the MMA latency (issue -> commit) is exposed: 306 cycles of S wait per
-//     entry and the issuer busy ~1620 cycles per entry for 1024 cycles of
-//     tensor work. A third S buffer (one shared O, row max exchanged between
-//     the warpgroups) is the next step.
+//   * correct: matches the default kernel (v8) to bf16 rounding on C1 and C2
+//     (dense and sparse; max |diff| 0.002-0.016) -- after two barrier-phase
+//     fixes: p_full per S buffer (a CTA's warpgroups can run ahead of the
+//     peer's) and pv_done per buffer (a waiter can lag a barrier by two PVs,
+//     beyond what one parity bit resolves);
+//   * slower: C3 38.5 vs 32.9 ms sparse, 122.8 vs 113.3 ms dense. Three S
+//     buffers hide the MMA latency (S wait 207-350 cycles per entry), but the
+//     two warpgroups exponentiate the two halves of the SAME tile at the same
+//     time, so each SM spends 1,024 MUFU cycles + ~570 of ld/max/exchange/
+//     pack/store per tile with nothing overlapping the non-MUFU part (v8's
+//     ping-pong overlaps it); and at C3 the pair computes every union entry
+//     for both rows (1.18x the MMAs). Next: exp2 partly on the FMA pipe (the
+//     FMA pipe is idle here) and staggering the warpgroups.
 // To try it: add it to build.py SOURCES, route launch_attn to
-// launch_attn_v11 and build the K tensor map with 64-row boxes.
+// launch_attn_v11 (FP_ATTN_VERSION 11) and build the K tensor map with 64-row
+// boxes (K is loaded in 64-key halves).
 // fp_attn11.cu -- stage (iii) of FlexPrefill, y = A(Q, K, V, S) (P:66-83,
 // P:287-288), version 11: a CTA PAIR (cluster of 2, cta_group::2 MMAs) per
-// q-block pair, one query row per SM, S double-buffered.
+// q-block pair, one query row per SM, S triple-buffered, one O.
 //
 // Why (profiles/r01_v8_phase_timing.txt, r01_dense_vs_cudnn.txt): in v8 each
 // of the two rows of a CTA has ONE S buffer in TMEM (S_A, S_B, O_A, O_B fill
@@ -26,21 +30,21 @@
 // MMA is one M = 256 cta_group::2 instruction: each SM holds its own 128 query
 // rows, HALF of each K tile (64 keys) and HALF of each V tile (64 of the 128
 // head dims), so
-//   * each SM's TMEM holds only its own row: S0, S1 (two S buffers), O0, O1;
-//   * S(e+1) is computed while the softmax of S(e) runs (no per-row stall);
+//   * each SM's TMEM holds only its own row: S0, S1, S2 (three S buffers)
+//     and O; S(e) is issued two entries ahead of its softmax;
 //   * K/V bytes per SM per entry halve (16 + 16 KiB) and so do the
 //     tensor-core shared-memory operand reads of B.
-// Union entries alternate between two softmax warpgroups (WG w takes entries
-// e = w mod 2 and owns S_w and O_w, with its own running max / sum); the two
-// partial softmaxes are merged in the epilogue (split-K style). Every union
-// entry is computed for BOTH rows (one M = 256 MMA): an entry the row did not
+// The two softmax warpgroups split every tile by keys (WG w: keys 64w..)
+// and exchange half-row maxima through shared memory each entry (one running
+// max, one O; WG w rescales and stores O's d-columns 64w..). Every union entry
+// is computed for BOTH rows (one M = 256 MMA): an entry the row did not
 // select gets P = 0 (no exponentials), so at C3 ~18% of the MMAs are spent
 // on unselected (row, entry) pairs (tools/pair_study.py: 1.69 computed tiles
 // per union entry); dense has one such tile per pair (the diagonal of row A).
 //
 // Roles (384 threads per CTA; the leader is cluster rank 0):
-//   warps 0-3  softmax WG0 (entries 0, 2, 4, ...)   one query row per thread
-//   warps 4-7  softmax WG1 (entries 1, 3, 5, ...)   (TMEM lane = row)
+//   warps 0-3  softmax WG0 (keys 0-63 of each tile)    one query row per thread
+//   warps 4-7  softmax WG1 (keys 64-127 of each tile)  (TMEM lane = row)
 //   warp 8     K producer (own half: keys 64r..64r+63 of the block)
 //   warp 9     TMEM allocation (both CTAs); MMA issuer (leader only)
 //   warp 10    V producer (own half: head dims 64r..64r+63)
@@ -73,7 +77,7 @@ namespace {
 constexpr int kThreads11 = 384;
 constexpr int kKS11 = 4, kVS11 = 4;          // K / V ring depths (half tiles)
 constexpr int kHalfBytes = kTileBytes / 2;   // 16 KiB: 64 keys x 128 d, or 128 keys x 64 d
-constexpr uint32_t kColS11 = 0, kColO11 = 256;
+constexpr uint32_t kColS11 = 0, kColO11 = 384;  // S0 S1 S2 | O
 constexpr float kRescale11 = 8.0f;
 
 struct Attn11Smem {
@@ -83,8 +87,12 @@ struct Attn11Smem {
   uint64_t q_full;
   uint64_t k_full[kKS11], k_empty[kKS11];
   uint64_t v_full[kVS11], v_empty[kVS11];
-  uint64_t s_full[2], p_full[2][2], pv_done[2];  // p_full[WG][buffer]
-  float m1[128], l1[128];             // WG1's running max / sum per row (epilogue merge)
+  // three S buffers (entry e in buffer e % 3): S(e) is issued two entries ahead
+  uint64_t s_full[3], p_full[2][3], pv_done[3];
+  // per-entry half-row maxima [e & 3][WG][row]: a WG can be up to three
+  // entries ahead of the other (unselected entries have no barrier)
+  float mxs[4][2][128];
+  float lsum[2][128];                 // final partial sums [WG][row]
   uint32_t tmem_base;
 };
 
@@ -296,14 +304,13 @@ __global__ void __launch_bounds__(kThreads11, 1)
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.v_empty[s], 1);
     }
-    for (int w = 0; w < 2; ++w) {
-      mbar_init(&sm.s_full[w], 1);
-      // 4 softmax warps of WG w in each of the 2 CTAs; one barrier per S buffer:
-      // a WG may finish entry e + 1 (S(e + 1) is issued before PV(e)) while the
-      // peer CTA's WG is still on entry e
-      mbar_init(&sm.p_full[w][0], 8);
-      mbar_init(&sm.p_full[w][1], 8);
-      mbar_init(&sm.pv_done[w], 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&sm.s_full[i], 1);
+      mbar_init(&sm.pv_done[i], 1);
+      // 4 softmax warps of WG w in each of the 2 CTAs; one barrier per S
+      // buffer: a CTA's WGs may run up to two entries ahead of the peer's
+      mbar_init(&sm.p_full[0][i], 8);
+      mbar_init(&sm.p_full[1][i], 8);
     }
     mbar_fence_init();
   }
@@ -360,23 +367,20 @@ __global__ void __launch_bounds__(kThreads11, 1)
         constexpr uint32_t idesc_o = make_idesc_bf16(256, 128, true);
         const uint64_t qdesc = sdesc_kmajor(smem_u32(sm.q), 0);
         FP_T11_DECL(true);
-        auto issue_pv = [&](int e) {  // O_w += P_w V_w(e) for both key halves w
+        auto issue_pv = [&](int e) {  // O += P(e) V(e): 8 k-steps, P of both halves at buffer cols 0..63
           const int vs = e % kVS11;
-          const uint32_t sb = tbase + kColS11 + (e & 1) * 128;
-          const uint64_t vdesc = make_sdesc(smem_u32(sm.v[vs]), kBoxBytes, 1024);
+          const int bf = e % 3;
           FP_T11(12);
           mbar_wait(&sm.v_full[vs], (e / kVS11) & 1);
           FP_T11(9);
-#pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            FP_T11(12);
-            mbar_wait(&sm.p_full[w][e & 1], (e >> 1) & 1);
-            FP_T11(10 + w);
-            tc_fence_after();
-            // keys 64w..64w+63: P at S columns 64w.., V rows 64w.. (k-steps 4w..)
-            umma2_ts_chain4(tbase + kColO11 + w * 128, sb + 64 * w, vdesc + 512 * w, idesc_o, e >= 1);
-            umma_commit_mc(&sm.pv_done[w]);
-          }
+          mbar_wait(&sm.p_full[0][bf], (e / 3) & 1);
+          FP_T11(10);
+          mbar_wait(&sm.p_full[1][bf], (e / 3) & 1);
+          FP_T11(11);
+          tc_fence_after();
+          umma2_ts_chain8(tbase + kColO11, tbase + kColS11 + bf * 128,
+                          make_sdesc(smem_u32(sm.v[vs]), kBoxBytes, 1024), idesc_o, e >= 1);
+          umma_commit_mc(&sm.pv_done[bf]);
           umma_commit_mc(&sm.v_empty[vs]);
         };
         mbar_wait(&sm.q_full, 0);
@@ -393,15 +397,15 @@ __global__ void __launch_bounds__(kThreads11, 1)
           ++tacc[14];
 #endif
           tc_fence_after();
-          // S(e) overwrites P(e - 2) in buffer e % 2: PV(e - 2) was issued in
-          // the previous iteration (one in-order tcgen05.mma stream); S(e) is
-          // computed while the softmax of S(e - 1) runs
-          umma2_ss_chain8(tbase + kColS11 + (e & 1) * 128, qdesc, make_sdesc(smem_u32(sm.k[ks]), 16, 1024),
+          // S(e) overwrites P(e - 3) in buffer e % 3: PV(e - 3) was issued in
+          // the previous iteration (one in-order tcgen05.mma stream)
+          umma2_ss_chain8(tbase + kColS11 + (e % 3) * 128, qdesc, make_sdesc(smem_u32(sm.k[ks]), 16, 1024),
                           idesc_s);
-          umma_commit_mc(&sm.s_full[e & 1]);
+          umma_commit_mc(&sm.s_full[e % 3]);
           umma_commit_mc(&sm.k_empty[ks]);
-          if (e >= 1) issue_pv(e - 1);
+          if (e >= 2) issue_pv(e - 2);
         }
+        if (e >= 2) issue_pv(e - 2);
         if (e >= 1) issue_pv(e - 1);
         FP_T11(12);
         FP_T11_FLUSH(8, 15);
@@ -410,11 +414,15 @@ __global__ void __launch_bounds__(kThreads11, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     // ------------------------------------------------ softmax warpgroups
-    const int w = wid >> 2;                    // WG: keys 64w..64w+63 of every tile
+    // WG w owns keys 64w..64w+63 of every S tile; the row max is combined
+    // across the two WGs each entry (one running max, one O)
+    const int w = wid >> 2;
     const int r = (wid & 3) * 32 + lane_id();  // query row within the block = TMEM lane
     const uint32_t lane_off = (uint32_t)((wid & 3) * 32) << 16;
-    const uint32_t tO = tbase + kColO11 + w * 128 + lane_off;
-    const uint32_t pbar0 = map_rank(&sm.p_full[w][0], 0), pbar1 = map_rank(&sm.p_full[w][1], 0);
+    const uint32_t tO = tbase + kColO11 + lane_off;
+    uint32_t pbar[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) pbar[i] = map_rank(&sm.p_full[w][i], 0);
     float m_used = -INFINITY, l = 0.f;
     UnionIter11 it{la, lb, nA, nB, 0, 0, DENSE};
     FP_T11_DECL(leader && (wid & 3) == 0 && lane_id() == 0);
@@ -422,14 +430,15 @@ __global__ void __launch_bounds__(kThreads11, 1)
     for (; !it.done(); ++e) {
       int mask;
       const int kb = it.next(mask);
-      const uint32_t tS = tbase + kColS11 + (e & 1) * 128 + 64 * w + lane_off;
-      mbar_wait(&sm.s_full[e & 1], (e >> 1) & 1);
+      const int bf = e % 3;
+      const uint32_t tSb = tbase + kColS11 + bf * 128 + lane_off;  // this buffer, lane base
+      mbar_wait(&sm.s_full[bf], (e / 3) & 1);
       FP_T11(0);
       tc_fence_after();
-      const bool sel = (mask >> rank) & 1;
+      const bool sel = (mask >> rank) & 1;  // same for every thread of the CTA
       if (sel) {
         float v[64];
-        tmem_ld_x64_11(tS, reinterpret_cast<uint32_t*>(v));
+        tmem_ld_x64_11(tSb + 64 * w, reinterpret_cast<uint32_t*>(v));
         tmem_wait_ld();
         if (kb == qbX) {  // the diagonal block: keys 64w + c <= r only
 #pragma unroll
@@ -445,28 +454,31 @@ __global__ void __launch_bounds__(kThreads11, 1)
           for (int q = 0; q < 4; ++q) mc[q] = fmax3_11(mc[q], v[16 * q + c], v[16 * q + c + 1]);
 #pragma unroll
         for (int q = 0; q < 4; ++q) mc[q] = fmaxf(mc[q], v[16 * q + 15]);
-        const float mx = fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])) * scale_log2;
-        // a fully masked half (diagonal, r < 64w) keeps alpha = 1 and gives P = 0
+        const float hm = fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3]));
+        // combine with the other half (both WGs have loaded S after this
+        // barrier, so WG1 may then store its P over WG0's half of S)
+        sm.mxs[e & 3][w][r] = hm;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const float mx = fmaxf(hm, sm.mxs[e & 3][w ^ 1][r]) * scale_log2;
         float alpha = 1.f;
         if (mx > m_used + kRescale11) {
           alpha = exp2f(m_used - mx);  // 0 on the first selected tile
           m_used = mx;
         }
-        // nothing seen yet (a fully masked diagonal half first): P = 0, not NaN
-        const float nm = m_used == -INFINITY ? 0.f : -m_used;
-        // rescale O_w before P(e) is released; PV_w(e - 1) was issued after
-        // S(e), so its completion is waited for here (only when needed)
+        const float nm = -m_used;
+        // rescale this WG's half of O (d-columns 64w..) before P(e) is
+        // released; PV(e - 1) may still be in flight: wait for it
         if (e > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          mbar_wait(&sm.pv_done[w], (e - 1) & 1);
+          mbar_wait(&sm.pv_done[(e - 1) % 3], ((e - 1) / 3) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
+          for (int q2 = 0; q2 < 2; ++q2) {
             uint32_t ov[32];
-            tmem_ld32(tO + q4 * 32, ov);
+            tmem_ld32(tO + 64 * w + q2 * 32, ov);
             tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
-            tmem_st32(tO + q4 * 32, ov);
+            tmem_st32(tO + 64 * w + q2 * 32, ov);
           }
         }
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
@@ -485,71 +497,59 @@ __global__ void __launch_bounds__(kThreads11, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) pk[c] = pack_bf16x2(v[c0 + 2 * c], v[c0 + 2 * c + 1]);
-          tmem_st16(tS + ch * 16, pk);  // P over this half of S: 32 keys = 16 columns
+          // P of keys 64w + c0.. at buffer columns 32w + c0/2 (bf16 pairs)
+          tmem_st16(tSb + 32 * w + ch * 16, pk);
         }
         l = l * alpha + ((s0 + s1) + (s2 + s3));
         FP_T11(1);
       } else {
         // entry of the other row only: P = 0 for this row (the M = 256 MMA
-        // covers both rows)
+        // covers both rows). WG1 writes over WG0's S half: fine, nobody reads
+        // S of an unselected entry.
         uint32_t z[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) z[c] = 0u;
-        tmem_st32(tS, z);
+        tmem_st32(tSb + 32 * w, z);
       }
       tmem_wait_st();
       FP_T11(2);
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive_remote((e & 1) ? pbar1 : pbar0);
+      if (lane_id() == 0) mbar_arrive_remote(pbar[bf]);
       FP_T11(3);
     }
-    // ---- epilogue: merge the two WGs' partial softmaxes, O / l -> global
     FP_T11_FLUSH(0, 8);
 #ifdef FP_TIMING
     if (t_on) atomicAdd(&g_attn11_timing[15], (unsigned long long)e);
 #endif
-    const int nw0 = e, nw1 = e;  // PVs into O0 / O1: one per union entry each
-    if (w == 1) {
-      sm.m1[r] = m_used;
-      sm.l1[r] = l;
-    }
+    // ---- epilogue: l = l0 + l1 (same running max); WG w stores d-columns 64w..
+    sm.lsum[w][r] = l;
     asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (w == 0 && qbX >= 0) {
-      if (nw0 > 0) mbar_wait(&sm.pv_done[0], (nw0 - 1) & 1);
-      if (nw1 > 0) mbar_wait(&sm.pv_done[1], (nw1 - 1) & 1);
+    if (qbX >= 0) {
+      // the last PV of each buffer residue (entries b, b + 3, ... < e)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int cnt = (e - b + 2) / 3;
+        if (cnt > 0) mbar_wait(&sm.pv_done[b], (cnt - 1) & 1);
+      }
       tc_fence_after();
-      const float m0 = m_used, l0 = l, m1 = sm.m1[r], l1 = sm.l1[r];
-      const float mm = fmaxf(m0, m1);
-      const float c0 = l0 > 0.f ? exp2f(m0 - mm) : 0.f;
-      const float c1 = l1 > 0.f ? exp2f(m1 - mm) : 0.f;
-      const float il = 1.0f / (l0 * c0 + l1 * c1);
-      const float f0 = c0 * il, f1 = c1 * il;
+      const float il = 1.0f / (sm.lsum[0][r] + sm.lsum[1][r]);
       const int row = qbX * 128 + r;
       const size_t off = toff(ol, h, row);
       uint4* dst = reinterpret_cast<uint4*>(o + off);
-      const uint32_t tO0 = tbase + kColO11 + lane_off, tO1 = tO0 + 128;
 #pragma unroll
-      for (int cb = 0; cb < 128; cb += 32) {
-        uint32_t a[32], b[32];
-        tmem_ld32(tO0 + cb, a);
-        tmem_ld32(tO1 + cb, b);
+      for (int cb = 0; cb < 64; cb += 32) {
+        uint32_t a[32];
+        tmem_ld32(tO + 64 * w + cb, a);
         tmem_wait_ld();
         if (row < n) {
 #pragma unroll
           for (int c = 0; c < 32; c += 8) {
             uint32_t wv[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int i0 = c + 2 * q, i1 = i0 + 1;
-              // a WG without a PV never wrote its O: select, never multiply garbage
-              const float x0 = (c0 > 0.f ? __uint_as_float(a[i0]) * f0 : 0.f) +
-                               (c1 > 0.f ? __uint_as_float(b[i0]) * f1 : 0.f);
-              const float x1 = (c0 > 0.f ? __uint_as_float(a[i1]) * f0 : 0.f) +
-                               (c1 > 0.f ? __uint_as_float(b[i1]) * f1 : 0.f);
-              wv[q] = pack_bf16x2(x0, x1);
-            }
-            dst[(cb + c) / 8] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            for (int q = 0; q < 4; ++q)
+              wv[q] = pack_bf16x2(__uint_as_float(a[c + 2 * q]) * il, __uint_as_float(a[c + 2 * q + 1]) * il);
+            dst[(64 * w + cb + c) / 8] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
           }
         }
       }
