@@ -28,7 +28,7 @@ namespace fp {
 namespace {
 
 constexpr int kRepThreads = 256;
-constexpr int kStages = 3;
+constexpr int kStages = 2;
 
 struct RepSmem {
   // tiles first (1024-B aligned by the dynamic smem base alignment)
@@ -42,7 +42,8 @@ struct RepSmem {
   float il_row[128];
   float red[512];
 };
-constexpr int kTStride = 129;  // pass-2 transpose buffer row stride (floats)
+// pass-2 slash partials: per warp, 4 column segments of 16, 47 diagonals each
+constexpr int kSeg = 4, kSegCols = 16, kSegDiag = kSegCols + 31, kSegStride = 48;
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -108,7 +109,7 @@ __device__ float block_max(float v, float* red) {
 // column = rep row r. Both are M=N=K=128 bf16 UMMAs on K-major SW128 tiles.
 // 8 warps: warp w reads TMEM lane quarter (w % 4) and column half (w / 4).
 template <int PASS>
-__global__ void __launch_bounds__(kRepThreads, 1)
+__global__ void __launch_bounds__(kRepThreads, 2)
     rep_pass(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
              int H, int G, int Hp, int Gp, int n, int nb, int nt, int bsz, int nchunks, int ct,
              float scale_log2,
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kRepThreads, 1)
   // SWIZZLE_128B tiles need 1024-B aligned shared addresses
   uint8_t* sbase = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   RepSmem& sm = *reinterpret_cast<RepSmem*>(sbase);
-  float* T = reinterpret_cast<float*>(sbase + sizeof(RepSmem));  // PASS 2 only
+  float* P2 = reinterpret_cast<float*>(sbase + sizeof(RepSmem));  // PASS 2 slash partials
 
   const int tid = threadIdx.x;
   const int wq = warp_id() & 3, half = warp_id() >> 2;
@@ -243,43 +244,60 @@ __global__ void __launch_bounds__(kRepThreads, 1)
     } else {
       // lane = key j_local, columns = rep rows r = half*64 .. half*64+63
       const int jl = lane_row;
-      const int j = tile * 128 + jl;
       float cs[4] = {0.f, 0.f, 0.f, 0.f};
-      float* Trow = T + jl * kTStride + half * 64;
-      if (half * 64 >= r_lo) {
+      // Slash partials without a transpose: diagonal delta = r - jl. A running
+      // sum that moves up one lane per column follows one diagonal of this
+      // warp's 32 x 64 sub-tile (lane L adds its p at column c to the run of
+      // delta_local = c - L). Four 16-column segments run as independent
+      // chains; lane 31 emits each finished run, the other lanes emit theirs
+      // after a segment's last column. Partials land in P2[warp][seg][idx],
+      // idx = delta_local - (16 seg - 31).
+      float* wp = P2 + warp_id() * (kSeg * kSegStride);
+      float run[kSeg] = {0.f, 0.f, 0.f, 0.f};
+      const bool active = half * 64 >= r_lo;  // rows outside Q^ (b = 64): no probability mass
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
+      for (int i = 0; i < kSegCols; ++i) {
+#pragma unroll
+        for (int sg = 0; sg < kSeg; ++sg) {
+          const int c = sg * kSegCols + i;
           const int r = half * 64 + c;
-          float p = fast_exp2(fmaf(__uint_as_float(v[c]), scale_log2, -sm.m_row[r])) * sm.il_row[r];
-          if (last && jl > lim + r) p = 0.f;
+          float p = 0.f;
+          if (active) {
+            p = fast_exp2(fmaf(__uint_as_float(v[c]), scale_log2, -sm.m_row[r])) * sm.il_row[r];
+            if (last && jl > lim + r) p = 0.f;
+          }
           cs[c & 3] += p;
-          Trow[c] = p;
+          run[sg] += p;
+          if (lane_id() == 31) wp[sg * kSegStride + i] = run[sg];
+          if (i + 1 < kSegCols) {
+            run[sg] = __shfl_up_sync(0xffffffffu, run[sg], 1);
+            if (lane_id() == 0) run[sg] = 0.f;
+          }
         }
-      } else {  // rows outside Q^ (b = 64): no probability mass
-#pragma unroll
-        for (int c = 0; c < 64; ++c) Trow[c] = 0.f;
       }
+#pragma unroll
+      for (int sg = 0; sg < kSeg; ++sg)
+        if (lane_id() < 31) wp[sg * kSegStride + kSegDiag - 1 - lane_id()] = run[sg];
       sm.red[half * 128 + jl] = (cs[0] + cs[1]) + (cs[2] + cs[3]);
       __syncthreads();
       if (tid < 128 && tile * 128 + tid < n)
         a_v[(size_t)h * n + tile * 128 + tid] = (sm.red[tid] + sm.red[128 + tid]) * inv_b;
-      (void)j;
-      // slash partials: diagonal delta = r - jl in [-127, 127], one per thread;
-      // offset o = p_r - j = (n - 128 - tile*128) + delta
+      // slash partial of diagonal dl = r - jl in [-127, 127] of this tile, one
+      // per thread, summed over the 8 warps and their segments in a fixed order;
+      // offset o = p_r - j = (n - 128 - tile*128) + dl
       if (tid < 255) {
         const int dl = tid - 127;
-        const int q0 = max(0, -dl), q1 = 128 - max(0, dl);
-        const float* tp = T + q0 * (kTStride + 1) + dl;
-        float s0 = 0.f, s1 = 0.f;
-        int q = q0;
-#pragma unroll 4
-        for (; q + 1 < q1; q += 2) {
-          s0 += tp[0];
-          s1 += tp[kTStride + 1];
-          tp += 2 * (kTStride + 1);
+        float acc = 0.f;
+#pragma unroll
+        for (int w8 = 0; w8 < 8; ++w8) {
+          const int dloc = dl - (w8 >> 2) * 64 + (w8 & 3) * 32;  // delta_local in warp w8
+#pragma unroll
+          for (int sg = 0; sg < kSeg; ++sg) {
+            const int idx = dloc - (sg * kSegCols - 31);
+            if (idx >= 0 && idx < kSegDiag) acc += P2[(w8 * kSeg + sg) * kSegStride + idx];
+          }
         }
-        if (q < q1) s0 += tp[0];
-        as_part[((size_t)h * nt + tile) * 256 + dl + 127] = s0 + s1;
+        as_part[((size_t)h * nt + tile) * 256 + dl + 127] = acc;
       }
     }
     tc_fence_before();
@@ -512,7 +530,7 @@ cudaStream_t plan_side_stream() {
 
 size_t rep_smem_bytes(int pass) {
   size_t b = sizeof(RepSmem);
-  if (pass == 2) b += (size_t)128 * kTStride * 4;
+  if (pass == 2) b += (size_t)8 * kSeg * kSegStride * 4;
   return b + 1024;  // slack for manual alignment
 }
 
