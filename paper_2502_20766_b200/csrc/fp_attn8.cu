@@ -189,6 +189,50 @@ FP_DEV void umma_pv_chain8(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc,
       "l"(b0 + 640), "l"(b0 + 768), "l"(b0 + 896), "r"(idesc), "r"(acc0));
 }
 
+// The MMA issuer runs as a whole warp (FP_WARPISSUE8, default): every lane
+// executes the same loop on the same (warp-uniform) values and the MMA /
+// commit instructions are predicated on elect.sync inside the asm. With the
+// issuer under `if (lane_id() == 0)` instead, the descriptors live in
+// per-thread registers and ptxas wraps every tcgen05.mma in an R2UR +
+// elect/branch loop: ~52 cycles to issue one MMA (tools/attn8_timing.py),
+// which made the single issuing thread the bottleneck of the kernel.
+#ifndef FP_WARPISSUE8
+#define FP_WARPISSUE8 1
+#endif
+constexpr bool kWarpIssue8 = FP_WARPISSUE8 != 0;
+#define FP_ELECT "elect.sync _|ep, 0xffffffff;\n\t"
+FP_DEV void umma_ss_chain8_w(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, 1, 0;\n\t" FP_ELECT
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %9, %17, 0;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %10, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %11, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %12, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %13, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %14, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %15, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %16, %17, p;\n\t}" ::"r"(d),
+      "l"(a0), "l"(a0 + 2), "l"(a0 + 4), "l"(a0 + 6), "l"(a0 + 1024), "l"(a0 + 1026),
+      "l"(a0 + 1028), "l"(a0 + 1030), "l"(b0), "l"(b0 + 2), "l"(b0 + 4), "l"(b0 + 6),
+      "l"(b0 + 1024), "l"(b0 + 1026), "l"(b0 + 1028), "l"(b0 + 1030), "r"(idesc));
+}
+FP_DEV void umma_pv_chain4_w(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q, ep;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t" FP_ELECT
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %9, q;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %6, %9, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %7, %9, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %8, %9, p;\n\t}" ::"r"(d),
+      "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "l"(b0), "l"(b0 + 128), "l"(b0 + 256),
+      "l"(b0 + 384), "r"(idesc), "r"(acc0));
+}
+FP_DEV void umma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred ep;\n\t" FP_ELECT
+      "@ep tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // Half of O += P V: 4 k-steps (64 keys) starting at P column a0 / V descriptor b0.
 FP_DEV void umma_pv_chain4(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
   asm volatile(
@@ -200,6 +244,10 @@ FP_DEV void umma_pv_chain4(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc,
       "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "l"(b0), "l"(b0 + 128), "l"(b0 + 256),
       "l"(b0 + 384), "r"(idesc), "r"(acc0));
 }
+
+#define PVCHAIN4(...) (kWarpIssue8 ? umma_pv_chain4_w(__VA_ARGS__) : umma_pv_chain4(__VA_ARGS__))
+#define SSCHAIN8(...) (kWarpIssue8 ? umma_ss_chain8_w(__VA_ARGS__) : umma_ss_chain8(__VA_ARGS__))
+#define COMMIT8(b) (kWarpIssue8 ? umma_commit_w(b) : umma_commit(b))
 
 // Merge of the two rows' sorted key-block lists: next union entry.
 // mask bit 0: row A selected it, bit 1: row B.
@@ -321,13 +369,13 @@ __global__ void __launch_bounds__(kThreads8, 1)
       }
     } else if (wid == 9) {
       // ------------------------------------------------ MMA issuer
-      if (lane_id() == 0) {
+      if (kWarpIssue8 || lane_id() == 0) {
         constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false);
         constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, true);
         const uint64_t qdesc[2] = {sdesc_kmajor(smem_u32(sm.q[0]), 0), sdesc_kmajor(smem_u32(sm.q[1]), 0)};
         int pend[2] = {-1, -1};  // union entry of X's S awaiting its PV
         int cnt[2] = {0, 0};     // S tiles issued per stream
-        FP_T8_DECL(true);
+        FP_T8_DECL(lane_id() == 0);
         auto issue_pv = [&](int x) {
           const int e = pend[x];
           const int vs = e % kVS8;
@@ -340,7 +388,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
             FP_T8(10);
             tc_fence_after();
 #if !defined(FP_XMMA8) && !defined(FP_XPV8)
-            umma_pv_chain4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
+            PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
                            cnt[x] > 1);
 #endif
             FP_T8(12);
@@ -348,7 +396,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
             FP_T8(11);
             tc_fence_after();
 #if !defined(FP_XMMA8) && !defined(FP_XPV8)
-            umma_pv_chain4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512,
+            PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512,
                            idesc_o, 1);
 #endif
           } else {
@@ -357,8 +405,8 @@ __global__ void __launch_bounds__(kThreads8, 1)
             umma_pv_chain8(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
                            cnt[x] > 1);
           }
-          umma_commit(&sm.v_empty[vs]);
-          umma_commit(&sm.pv_done[x]);
+          COMMIT8(&sm.v_empty[vs]);
+          COMMIT8(&sm.pv_done[x]);
           pend[x] = -1;
         };
         mbar_wait(&sm.q_full, 0);
@@ -379,18 +427,20 @@ __global__ void __launch_bounds__(kThreads8, 1)
           for (int x = 0; x < 2; ++x) {
             if (pend[x] >= 0) issue_pv(x);
             if (mask & (1 << x)) {
+              FP_T8(12);
 #if !defined(FP_XMMA8) && !defined(FP_XS8)
-              umma_ss_chain8(tbase + kColS8 + x * 128, qdesc[x], kdesc, idesc_s);
+              SSCHAIN8(tbase + kColS8 + x * 128, qdesc[x], kdesc, idesc_s);
 #endif
-              umma_commit(&sm.s_full[x]);
+              FP_T8(13);  // issue time of the 8 S MMAs
+              COMMIT8(&sm.s_full[x]);
               pend[x] = e;
               ++cnt[x];
             }
           }
-          umma_commit(&sm.k_empty[ks]);
+          COMMIT8(&sm.k_empty[ks]);
           // an entry only one row uses gets its second V-slot release here
           // (it arrives early, but the phase also needs the PV's commit)
-          if (mask != 3) umma_commit(&sm.v_empty[e % kVS8]);
+          if (mask != 3) COMMIT8(&sm.v_empty[e % kVS8]);
         }
         if (pend[0] >= 0) issue_pv(0);
         if (pend[1] >= 0) issue_pv(1);
@@ -455,10 +505,10 @@ __global__ void __launch_bounds__(kThreads8, 1)
         // O_X holds sum_{earlier} P V: PV of the previous tile completed before
         // S of this one (one in-order tcgen05.mma stream), so O can be
         // rescaled now, before PV's first half is released
-        // (pv_done is waited for only when O is touched: the barrier cannot run
-        // ahead of this thread, PV(t) needs this tile's P)
+        // every pv_done phase is consumed (here, normally long complete; an
+        // unconsumed phase is what compute-sanitizer synccheck reports)
+        if (t > 0) mbar_wait(&sm.pv_done[x], (t - 1) & 1);
         if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          mbar_wait(&sm.pv_done[x], (t - 1) & 1);
           {
             tc_fence_after();
 #pragma unroll

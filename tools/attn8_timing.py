@@ -53,7 +53,7 @@ tot = sum(buf[i] for i in names)
 for i, nm in names.items():
     print(f"  softmax {nm:16s} {buf[i] / tiles:8.1f} cyc/tile  {100 * buf[i] / max(tot, 1):5.1f}%")
 print(f"  softmax total            {tot / tiles:8.1f} cyc/tile")
-inames = {8: "wait K", 9: "wait V", 10: "wait P lo" if not a.v11 else "wait P WG0", 11: "wait P hi" if not a.v11 else "wait P WG1", 12: "issue/other"}
+inames = {8: "wait K", 9: "wait V", 10: "wait P lo" if not a.v11 else "wait P WG0", 11: "wait P hi" if not a.v11 else "wait P WG1", 12: "issue/other", 13: "S chain issue"}
 itot = sum(buf[i] for i in inames)
 for i, nm in inames.items():
     print(f"  issuer  {nm:16s} {buf[i] / ents:8.1f} cyc/entry  {100 * buf[i] / max(itot, 1):5.1f}%")
