@@ -205,6 +205,32 @@ FP_DEV void umma_commit(uint64_t* bar) {
 FP_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 FP_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// M=128 N=128 SS chain of 8 k-steps on K-major SW128 tiles of two 16 KiB boxes
+// (k-step kk at box kk/4, +32 B per step), issued by ONE elected lane of a
+// warp whose lanes all execute this with the same operands (keeps them in
+// uniform registers: no per-MMA R2UR / branch loop).
+FP_DEV void umma_ss_chain8_elect(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, 1, 0;\n\telect.sync _|ep, 0xffffffff;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %9, %17, 0;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %10, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %11, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %12, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %13, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %14, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %15, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %16, %17, p;\n\t}" ::"r"(d),
+      "l"(a0), "l"(a0 + 2), "l"(a0 + 4), "l"(a0 + 6), "l"(a0 + 1024), "l"(a0 + 1026),
+      "l"(a0 + 1028), "l"(a0 + 1030), "l"(b0), "l"(b0 + 2), "l"(b0 + 4), "l"(b0 + 6),
+      "l"(b0 + 1024), "l"(b0 + 1026), "l"(b0 + 1028), "l"(b0 + 1030), "r"(idesc));
+}
+FP_DEV void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred ep;\n\telect.sync _|ep, 0xffffffff;\n\t"
+      "@ep tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // ------------------------------------------------------------- TMEM --------
 // Called by one full warp. Writes the allocated base column address to *dst.
 FP_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {

@@ -155,18 +155,16 @@ __global__ void __launch_bounds__(kRepThreads, 2)
   const uint32_t tbase = sm.tmem_base;
   constexpr uint32_t idesc = make_idesc_bf16(128, 128, false);
 
+  // issued by all of warp 0 (warp-uniform operands, elect.sync inside the
+  // asm): a lane-0 issue loop cost ~50-130 cycles per MMA in R2UR / branch
+  // overhead, and warp 0 also does softmax work the whole CTA waits for
   auto issue_mma = [&](int t) {
     const int s = t % kStages, b = t & 1;
     mbar_wait(&sm.k_full[s], (t / kStages) & 1);
     tc_fence_after();
-    const uint32_t qa = smem_u32(sm.qhat), ka = smem_u32(sm.kst[s]);
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      uint64_t ad = PASS == 1 ? sdesc_kmajor(qa, kk) : sdesc_kmajor(ka, kk);
-      uint64_t bd = PASS == 1 ? sdesc_kmajor(ka, kk) : sdesc_kmajor(qa, kk);
-      umma_bf16_ss(tbase + b * 128, ad, bd, idesc, kk > 0);
-    }
-    umma_commit(&sm.mma_done[b]);
+    const uint64_t qd = sdesc_kmajor(smem_u32(sm.qhat), 0), kd = sdesc_kmajor(smem_u32(sm.kst[s]), 0);
+    umma_ss_chain8_elect(tbase + b * 128, PASS == 1 ? qd : kd, PASS == 1 ? kd : qd, idesc);
+    umma_commit_elect(&sm.mma_done[b]);
   };
 
   if (tid == 0) {
@@ -176,6 +174,9 @@ __global__ void __launch_bounds__(kRepThreads, 2)
       mbar_arrive_expect_tx(&sm.k_full[s], kTileBytes);
       tma_tile(sm.kst[s], &kmap, &sm.k_full[s], (t0 + s) * 128, g, Gp);
     }
+  }
+  if (warp_id() == 0) {
+    __syncwarp();
     mbar_wait(&sm.q_full, 0);
     issue_mma(0);
   }
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(kRepThreads, 2)
   float m_loc = -INFINITY, l_loc = 0.f;  // PASS 1 running row stats of this column half (log2)
 
   for (int t = 0; t < ntile; ++t) {
-    if (tid == 0 && t + 1 < ntile) issue_mma(t + 1);
+    if (warp_id() == 0 && t + 1 < ntile) issue_mma(t + 1);
     const int b = t & 1;
     const int tile = t0 + t;
     // key tile*128 + c is visible from rep row r iff c <= lim + r (p_r = n-128+r);
