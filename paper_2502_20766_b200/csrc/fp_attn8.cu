@@ -475,6 +475,10 @@ __global__ void __launch_bounds__(kThreads8, 1)
       float v[128];
       tmem_ld_32x32b_x64_8(tS, reinterpret_cast<uint32_t*>(v));
       tmem_ld_32x32b_x64_8(tS + 64, reinterpret_cast<uint32_t*>(v + 64));
+      // probe pv_done(t - 1) now (complete: S(t) followed PV(t - 1) in the
+      // in-order MMA stream) so the probe's latency overlaps the TMEM load;
+      // the phase is still consumed below, the loop only runs if it failed
+      const bool pv_ok = t == 0 || mbar_try_wait(smem_u32(&sm.pv_done[x]), (t - 1) & 1);
       tmem_wait_ld();
       FP_T8(1);
       if (t == nX - 1) {  // the diagonal block: keys j <= r only
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
         // rescaled now, before PV's first half is released
         // every pv_done phase is consumed (here, normally long complete; an
         // unconsumed phase is what compute-sanitizer synccheck reports)
-        if (t > 0) mbar_wait(&sm.pv_done[x], (t - 1) & 1);
+        if (!pv_ok) mbar_wait(&sm.pv_done[x], (t - 1) & 1);
         if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           {
             tc_fence_after();
