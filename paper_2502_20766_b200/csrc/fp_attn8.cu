@@ -73,7 +73,8 @@ constexpr float kRescale8 = 8.0f;  // lazy rescale: tolerate P up to 2^8 (as v5)
 constexpr int kEmu8 = FP_EMU8;
 // P handed to the tensor core in two halves (keys 0-63, 64-127): the softmax
 // stores P in 32-key chunks as the exponentials finish (tcgen05.st overlaps
-// the next chunk's MUFU work) and arrives on p_lo after the first half, so
+// the next chunk's MUFU work) and arrives on p_lo once the first half is
+// stored (checked after chunk 2's exponentials, so the wait does not stall), so
 // the issuer starts PV's first four k-steps while the second half is still
 // being exponentiated. Bitwise equal to the unsplit path; measured (C3,
 // alternating 12-launch blocks) 34.04-34.19 ms vs 34.20-34.79 ms sparse, equal
@@ -552,14 +553,16 @@ __global__ void __launch_bounds__(kThreads8, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) pk[c] = pack_bf16x2(v[c0 + 2 * c], v[c0 + 2 * c + 1]);
-          tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
-          if (ch == 1) {
+          // p_lo after chunk 2's exponentials: the stores of chunks 0-1 have
+          // completed by then, so the wait does not stall the MUFU stream
+          if (ch == 2) {
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(&sm.p_lo[x]);
             FP_T8(4);
           }
+          tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
         }
         l = l * alpha + ((s0 + s1) + (s2 + s3));
         tmem_wait_st();
