@@ -62,19 +62,21 @@ FP_DEV float quad_sum64(float v) {
 }
 
 // 8 k-steps of an M=128 x N=128 MMA in one asm statement, A from TMEM columns
-// a0 + 8 kk, B descriptors b0 + off(kk) (16-B units)
+// a0 + 8 kk, B descriptors b0 + off(kk) (16-B units). Executed by the whole
+// issuing warp (warp-uniform operands); one elected lane issues.
 template <uint32_t O1, uint32_t O2, uint32_t O3, uint32_t O4, uint32_t O5, uint32_t O6, uint32_t O7>
 FP_DEV void umma_ts_chain8_64(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
   asm volatile(
-      "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %18, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %9, %17, q;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %10, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %11, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %12, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %13, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %14, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %15, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %16, %17, p;\n\t}" ::"r"(d),
+      "{\n\t.reg .pred p, q, ep;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %18, 0;\n\t"
+      "elect.sync _|ep, 0xffffffff;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %9, %17, q;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %10, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %11, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %12, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %13, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %14, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %15, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %16, %17, p;\n\t}" ::"r"(d),
       "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "r"(a0 + 32), "r"(a0 + 40), "r"(a0 + 48),
       "r"(a0 + 56), "l"(b0), "l"(b0 + O1), "l"(b0 + O2), "l"(b0 + O3), "l"(b0 + O4), "l"(b0 + O5),
       "l"(b0 + O6), "l"(b0 + O7), "r"(idesc), "r"(acc0));
@@ -243,8 +245,9 @@ __global__ void __launch_bounds__(kThreads64, 1)
         for (int d = max(0, e - kKV64); d < e; ++d) mbar_wait(&empty[d % kKV64], (d / kKV64) & 1);
       }
     } else if (wid == 9) {
-      // ------------------------------------------------ MMA issuer
-      if (lane_id() == 0) {
+      // ------------------------------------------------ MMA issuer (whole warp,
+      // elect.sync-predicated MMA / commit / copy, as fp_attn8.cu)
+      {
         constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false);
         constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, true);
         const uint32_t qs = smem_u32(sm.q);
@@ -259,14 +262,15 @@ __global__ void __launch_bounds__(kThreads64, 1)
           tc_fence_after();
           umma_ts_chain8_64<FP64_KMAJ_OFFS>(tbase + b * 128, tbase + kColQ64,
                                             sdesc_kmajor(smem_u32(sm.k[s]), 0), idesc_s, 0);
-          umma_commit(&sm.s_full[b]);
-          umma_commit(&sm.k_empty[s]);
+          umma_commit_elect(&sm.s_full[b]);
+          umma_commit_elect(&sm.k_empty[s]);
         };
         mbar_wait(&sm.q_full, 0);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // Q -> TMEM columns kColQ64 + 8 kk
-          asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(tbase + kColQ64 + kk * 8),
+          asm volatile("{\n\t.reg .pred ep;\n\telect.sync _|ep, 0xffffffff;\n\t"
+                       "@ep tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(tbase + kColQ64 + kk * 8),
                        "l"(sdesc_kmajor(qs, kk)));
         issue_s();
         if (!it.done()) issue_s();
@@ -277,8 +281,8 @@ __global__ void __launch_bounds__(kThreads64, 1)
           tc_fence_after();
           umma_ts_chain8_64<FP64_MNMAJ_OFFS>(tbase + kColO64, tbase + b * 128,
                                              sdesc_mnmajor(smem_u32(sm.v[s]), 0), idesc_o, i > 0);
-          umma_commit(&sm.pv_done[b]);
-          umma_commit(&sm.v_empty[s]);
+          umma_commit_elect(&sm.pv_done[b]);
+          umma_commit_elect(&sm.v_empty[s]);
           if (!it.done()) issue_s();
         }
       }

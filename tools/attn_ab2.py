@@ -21,6 +21,7 @@ ap.add_argument("--workload", default="C3-llama8b-128k")
 ap.add_argument("--gamma", type=float, default=None)
 ap.add_argument("--reps", type=int, default=12)
 ap.add_argument("--dense", action="store_true")
+ap.add_argument("--block", type=int, default=128)
 ap.add_argument("--blocks", type=int, default=3)
 ap.add_argument("--block-len", type=int, default=12)
 a = ap.parse_args()
@@ -33,7 +34,7 @@ w = configs.get(a.workload)
 if a.gamma is not None:
     w = w.with_(gamma=a.gamma)
 q, k, v = (torch.from_numpy(x).view(torch.bfloat16).cuda() for x in gen.make_layer_bits(w))
-fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len)
+fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len, block_size=a.block)
 out = torch.empty_like(q)
 fpl.plan(q, k, w.tau)
 fpl.select(w.gamma, w.min_budget)
@@ -53,7 +54,7 @@ def call(L):
                                    w.kv_heads, w.seq_len, 128, 128, None, 0, st)
     else:
         r = L.fp_sparse_attn(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), w.heads,
-                             w.kv_heads, w.seq_len, 128, 128, fpl.row_ptr.data_ptr(),
+                             w.kv_heads, w.seq_len, 128, a.block, fpl.row_ptr.data_ptr(),
                              fpl.col_idx.data_ptr(), fpl.ws.data_ptr(), fpl.ws_bytes, st)
     assert r == 0, r
 
