@@ -26,7 +26,8 @@
  *    says host. The caller owns all memory; the library never allocates device
  *    memory, keeps no per-call state, and only enqueues work ordered on `stream`
  *    (no host syncs; fp_plan at short lengths forks one branch onto an internal
- *    per-device side stream and joins it back through events before returning), so
+ *    side stream, one per calling thread and device, and joins it back through
+ *    events before returning), so
  *    fp_plan -> fp_select -> fp_sparse_attn is CUDA-graph capturable. Stages
  *    communicate through the workspace; data-dependent sizes stay on device.
  *  - Validation is synchronous and happens before anything is enqueued; an
@@ -181,8 +182,10 @@ fp_status fp_select(int heads, int kv_heads, int seq_len, int head_dim, int bloc
                     fp_select_stats* stats, void* stream);
 
 /* fp_select with the selection variants of fp_select_options (NULL = the
- * defaults, identical to fp_select). FP_ERR_RANGE for a mode outside {0, 1} or
- * max_budget < 0. */
+ * defaults, identical to fp_select). FP_ERR_RANGE for a mode outside {0, 1},
+ * max_budget < 0, or 0 < max_budget < min_budget (the cap is applied after the
+ * floor, A23, and may not undercut it). Token budgets are converted to blocks
+ * in 64-bit arithmetic and clamped to nb. */
 fp_status fp_select_ex(int heads, int kv_heads, int seq_len, int head_dim, int block_size,
                        float gamma, int min_budget, const fp_select_options* opt, void* ws,
                        size_t ws_bytes, int32_t* row_ptr, int32_t* col_idx, fp_select_stats* stats,
@@ -193,7 +196,9 @@ fp_status fp_select_ex(int heads, int kv_heads, int seq_len, int head_dim, int b
  *   o         device bf16 [heads][seq_len][128] out
  *   row_ptr, col_idx  the CSR from fp_select (or any CSR with kb <= qb, each row
  *             containing its diagonal block qb, kb ascending)
- *   ws        workspace (scheduler scratch)
+ *   ws        optional scheduler scratch: NULL, or a workspace of this shape
+ *             (16-B aligned, ws_bytes >= fp_workspace_bytes(...), else
+ *             FP_ERR_ALIGN / FP_ERR_WORKSPACE); the output does not depend on it
  */
 fp_status fp_sparse_attn(const void* q, const void* k, const void* v, void* o, int heads,
                          int kv_heads, int seq_len, int head_dim, int block_size,
@@ -247,7 +252,13 @@ fp_status fp_dense_causal_attn_ex(const void* q, const void* k, const void* v, v
  * copy of group c+1 and the device->host copy of group c-1 overlap the compute
  * of group c on internal streams, joined back into `stream` before return
  * (ws must hold fp_workspace_bytes of the whole layer; pattern, jsd, row_ptr,
- * col_idx are the full-layer arrays). Overlap needs pinned host buffers. */
+ * col_idx are the full-layer arrays). Overlap needs pinned host buffers.
+ * The results are bitwise those of fp_plan / fp_select / fp_sparse_attn on the
+ * whole layer. Every argument (pointers, 16-B alignment of the device buffers
+ * and ws, 4-B alignment of pattern / jsd / row_ptr / col_idx, shape, ranges,
+ * workspace size, device) is validated before the first copy is enqueued.
+ * The internal streams and events are created once per (calling thread,
+ * device) and reused; calls from different threads never share them. */
 fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_host, void* o_host,
                         void* d_q, void* d_k, void* d_v, void* d_o, int heads, int kv_heads,
                         int seq_len, int head_dim, int block_size, float gamma, float tau,

@@ -256,6 +256,11 @@ def fp_debug_view(ws, heads, kv_heads, seq_len, head_dim=128, block_size=128):
 
 
 # ------------------------------------------------------------ convenience ---
+# The paper's defaults: block 128, tau 0.1, every head computes at
+# least 1024 tokens (minimum budget; per query-block row in kernel units, A12).
+PAPER_MIN_BUDGET = 1024
+
+
 class FlexPrefill:
     """Owns the workspace and CSR buffers for one (heads, kv_heads, seq_len) shape.
 
@@ -297,7 +302,7 @@ class FlexPrefill:
         fp_plan(q, k, self.H, self.G, self.n, tau, self.ws, self.ws_bytes, self.pattern, self.jsd,
                 stream, block_size=self.b)
 
-    def select(self, gamma=0.95, min_budget=0, stream=None, with_stats=True, vs_mode=0, qa_mode=0,
+    def select(self, gamma=0.95, min_budget=PAPER_MIN_BUDGET, stream=None, with_stats=True, vs_mode=0, qa_mode=0,
                max_budget=0):
         fp_select_ex(self.H, self.G, self.n, gamma, min_budget, self.ws, self.ws_bytes,
                      self.row_ptr, self.col_idx, self.stats_buf if with_stats else None, stream,
@@ -320,12 +325,12 @@ class FlexPrefill:
         fp_dense_causal_attn(q, k, v, out, self.H, self.G, self.n, self.ws, self.ws_bytes, stream,
                              block_size=self.b)
 
-    def layer(self, q, k, v, out, gamma=0.95, tau=0.1, min_budget=0, stream=None):
+    def layer(self, q, k, v, out, gamma=0.95, tau=0.1, min_budget=PAPER_MIN_BUDGET, stream=None):
         self.plan(q, k, tau, stream)
         self.select(gamma, min_budget, stream, with_stats=False)
         self.attn(q, k, v, out, stream)
 
-    def capture_layer(self, q, k, v, out, gamma=0.95, tau=0.1, min_budget=0):
+    def capture_layer(self, q, k, v, out, gamma=0.95, tau=0.1, min_budget=PAPER_MIN_BUDGET):
         """Record plan -> select -> attn into one CUDA graph (the C ABI only
         enqueues on the current stream, so the whole layer is capturable).
         Returns the torch.cuda.CUDAGraph; replay() reruns the layer on the

@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <mutex>
+#include <vector>
 
 #include "fp_internal.h"
 
@@ -39,6 +40,25 @@ bool make_tile_map(CUtensorMap* map, const void* base, const TLayout& t, int n, 
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  struct Done {
+    const void* fn;
+    int dev;
+    size_t bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Done> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Done& d : done)
+    if (d.fn == fn && d.dev == dev && d.bytes >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.push_back(Done{fn, dev, bytes});
+  return e;
 }
 
 static fp_status check_shape(int heads, int kv_heads, int seq_len, int head_dim, int block_size) {
@@ -188,6 +208,9 @@ fp_status fp_select_ex(int heads, int kv_heads, int seq_len, int head_dim, int b
   if (opt_in) opt = *opt_in;
   if (opt.vs_mode < 0 || opt.vs_mode > 1 || opt.qa_mode < 0 || opt.qa_mode > 1 || opt.max_budget < 0)
     return FP_ERR_RANGE;
+  // the maximum budget is applied after the minimum one (A23): a cap below the
+  // floor would silently break the per-row minimum, so it is an error
+  if (opt.max_budget > 0 && opt.max_budget < min_budget) return FP_ERR_RANGE;
   if (!aligned16(ws)) return FP_ERR_ALIGN;
   const Shape s = make_shape(heads, kv_heads, seq_len, block_size);
   const WsLayout L = ws_layout(s);
@@ -212,10 +235,13 @@ static fp_status attn_common(const void* q, const void* k, const void* v, void* 
   Layout lay;
   if ((st = to_layout(layout, heads, kv_heads, seq_len, &lay))) return st;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return FP_ERR_ALIGN;
-  (void)ws_bytes;
-  if ((st = check_device())) return st;
   const Shape s = make_shape(lay.batch * heads, lay.batch * kv_heads, seq_len, block_size);
   const WsLayout L = ws_layout(s);
+  // ws is optional (scheduler scratch): NULL = no scratch; otherwise it must be
+  // a full workspace of this shape
+  if (ws && !aligned16(ws)) return FP_ERR_ALIGN;
+  if (ws && ws_bytes < L.total) return FP_ERR_WORKSPACE;
+  if ((st = check_device())) return st;
   CUtensorMap qm, km, vm;
   if (!make_tile_map(&qm, q, lay.q, seq_len, lay.batch) ||
       !make_tile_map(&km, k, lay.k, seq_len, lay.batch, attn_kv_box_rows()) ||
@@ -265,11 +291,48 @@ fp_status fp_dense_causal_attn_ex(const void* q, const void* k, const void* v, v
                      nullptr, ws, ws_bytes, stream, true);
 }
 
+namespace fp {
+// Streams and events of fp_layer_host, created on first use per (calling
+// thread, device) and reused by every later call of that thread: no per-call
+// create / destroy, and calls from different threads never share them.
+// Events are re-recorded freely: cudaStreamWaitEvent captures the event's most
+// recent record at the time of the wait call.
+struct HostPipe {
+  cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
+  cudaEvent_t ev[6] = {};  // start, done, kq, v, head, comp
+  bool ok = false;
+  ~HostPipe() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (sin) cudaStreamDestroy(sin);
+    if (scomp) cudaStreamDestroy(scomp);
+    if (sout) cudaStreamDestroy(sout);
+  }
+};
+static HostPipe* host_pipe() {
+  thread_local HostPipe pipes[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  HostPipe& p = pipes[dev];
+  if (!p.ok) {
+    bool good = cudaStreamCreateWithFlags(&p.sin, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&p.scomp, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaStreamCreateWithFlags(&p.sout, cudaStreamNonBlocking) == cudaSuccess;
+    for (cudaEvent_t& e : p.ev) good = good && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    if (!good) return nullptr;  // partially created handles are reused on the next try
+    p.ok = true;
+  }
+  return &p;
+}
+static bool aligned4(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 3u) == 0; }
+}  // namespace fp
+
 fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_host, void* o_host,
                         void* d_q, void* d_k, void* d_v, void* d_o, int heads, int kv_heads,
                         int seq_len, int head_dim, int block_size, float gamma, float tau,
                         int min_budget, void* ws, size_t ws_bytes, int32_t* pattern, float* jsd,
                         int32_t* row_ptr, int32_t* col_idx, void* stream) {
+  // ---- every check of the nested calls, up front: an invalid call enqueues nothing
   if (!q_host || !k_host || !v_host || !o_host || !d_q || !d_k || !d_v || !d_o || !ws || !pattern ||
       !jsd || !row_ptr || !col_idx)
     return FP_ERR_NULL;
@@ -277,38 +340,39 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
   if (st) return st;
   if (!(gamma > 0.f) || isnan(gamma) || !(tau >= 0.f && tau <= 1.f) || min_budget < 0)
     return FP_ERR_RANGE;
+  if (!aligned16(d_q) || !aligned16(d_k) || !aligned16(d_v) || !aligned16(d_o) || !aligned16(ws) ||
+      !aligned4(pattern) || !aligned4(jsd) || !aligned4(row_ptr) || !aligned4(col_idx))
+    return FP_ERR_ALIGN;
   if (ws_bytes < fp_workspace_bytes(heads, kv_heads, seq_len, head_dim, block_size))
     return FP_ERR_WORKSPACE;
   if ((st = check_device())) return st;
+  HostPipe* hp = host_pipe();
+  if (!hp) return cuda_status(cudaErrorUnknown);
   // Pipelined per chunk of Q heads (a KV group, g = heads / kv_heads Q heads +
   // their K/V; the first group split into single heads): host->device copies of
   // chunk c+1 and the device->host copies of chunk c-1 overlap the compute of
   // chunk c (three streams joined back to `stream`). Chunks alternate between
-  // two workspace slots (the full-layer workspace holds at least two).
+  // two workspace slots (the full-layer workspace holds at least two). Results
+  // are bitwise those of the single whole-layer call: heads are independent and
+  // no kernel's arithmetic depends on how many heads a call batches.
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  cudaStream_t sin = hp->sin, scomp = hp->scomp, sout = hp->sout;
+  cudaEvent_t e_start = hp->ev[0], e_done = hp->ev[1], e_kq = hp->ev[2], e_v = hp->ev[3],
+              e_h = hp->ev[4], e_c = hp->ev[5];
   const int g = heads / kv_heads;
   const size_t n = (size_t)seq_len, nb = (n + block_size - 1) / block_size, cap = nb * (nb + 1) / 2;
   const size_t qb_bytes = (size_t)g * n * 128 * 2, kv_bytes = n * 128 * 2;
   const size_t slot = align256(fp_workspace_bytes(g, 1, seq_len, head_dim, block_size));
   const int nslots = (kv_heads > 1 && ws_bytes >= 2 * slot) ? 2 : 1;
-  cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
-  cudaEvent_t e_start = nullptr, e_done = nullptr;
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) {
     if (e == cudaSuccess && r != cudaSuccess) e = r;
     return e == cudaSuccess;
   };
-  chk(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
-  chk(cudaStreamCreateWithFlags(&scomp, cudaStreamNonBlocking));
-  chk(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
-  chk(cudaEventCreateWithFlags(&e_start, cudaEventDisableTiming));
-  chk(cudaEventCreateWithFlags(&e_done, cudaEventDisableTiming));
-  if (e == cudaSuccess) {
-    chk(cudaEventRecord(e_start, cs));
-    chk(cudaStreamWaitEvent(sin, e_start, 0));
-    chk(cudaStreamWaitEvent(scomp, e_start, 0));
-    chk(cudaStreamWaitEvent(sout, e_start, 0));
-  }
+  chk(cudaEventRecord(e_start, cs));
+  chk(cudaStreamWaitEvent(sin, e_start, 0));
+  chk(cudaStreamWaitEvent(scomp, e_start, 0));
+  chk(cudaStreamWaitEvent(sout, e_start, 0));
   // Chunks of Q heads: the first KV group one head at a time (only its K + one
   // head of Q is uploaded before compute starts), every later group whole.
   struct Chunk {
@@ -333,15 +397,12 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
     // attention runs one launch per head (bitwise the same result: work items
     // are per (head, query block)) and each head's output is copied back as
     // soon as it is done, so only the last head's D2H is exposed at the end.
-    cudaEvent_t e_kq = nullptr, e_v = nullptr;
-    chk(cudaEventCreateWithFlags(&e_kq, cudaEventDisableTiming));
-    chk(cudaEventCreateWithFlags(&e_v, cudaEventDisableTiming));
     if (first_of_group) chk(cudaMemcpyAsync(kd, kh, kv_bytes, cudaMemcpyHostToDevice, sin));
     chk(cudaMemcpyAsync(qd, qh, ch.nh * hb, cudaMemcpyHostToDevice, sin));
     chk(cudaEventRecord(e_kq, sin));
     if (first_of_group) chk(cudaMemcpyAsync(vd, vh, kv_bytes, cudaMemcpyHostToDevice, sin));
-    chk(cudaEventRecord(e_v, sin));
     chk(cudaStreamWaitEvent(scomp, e_kq, 0));
+    chk(cudaEventRecord(e_v, sin));
     void* wsc = static_cast<char*>(ws) + (ci_ % nslots) * slot;
     const int hg = c * g + ch.h0;  // first global head of the chunk
     int32_t* rp = row_ptr + (size_t)hg * (nb + 1);
@@ -354,33 +415,19 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
     chk(cudaStreamWaitEvent(scomp, e_v, 0));
     for (int i = 0; i < ch.nh && e == cudaSuccess && st == FP_OK; ++i) {
       st = fp_sparse_attn(qd + i * hb, kd, vd, od + i * hb, 1, 1, seq_len, head_dim, block_size,
-                          rp + (size_t)i * (nb + 1), ci + (size_t)i * cap, wsc, slot, scomp);
-      cudaEvent_t e_h = nullptr;
-      chk(cudaEventCreateWithFlags(&e_h, cudaEventDisableTiming));
+                          rp + (size_t)i * (nb + 1), ci + (size_t)i * cap, nullptr, 0, scomp);
       chk(cudaEventRecord(e_h, scomp));
       chk(cudaStreamWaitEvent(sout, e_h, 0));
       chk(cudaMemcpyAsync(static_cast<char*>(o_host) + c * qb_bytes + (ch.h0 + i) * hb, od + i * hb,
                           hb, cudaMemcpyDeviceToHost, sout));
-      if (e_h) cudaEventDestroy(e_h);
     }
-    if (e_kq) cudaEventDestroy(e_kq);
-    if (e_v) cudaEventDestroy(e_v);
   }
-  // join everything back into the caller's stream
-  if (e == cudaSuccess) {
-    cudaEvent_t e_c = nullptr;
-    chk(cudaEventCreateWithFlags(&e_c, cudaEventDisableTiming));
-    chk(cudaEventRecord(e_c, scomp));
-    chk(cudaStreamWaitEvent(sout, e_c, 0));
-    chk(cudaEventRecord(e_done, sout));
-    chk(cudaStreamWaitEvent(cs, e_done, 0));
-    if (e_c) cudaEventDestroy(e_c);
-  }
-  if (sin) cudaStreamDestroy(sin);
-  if (scomp) cudaStreamDestroy(scomp);
-  if (sout) cudaStreamDestroy(sout);
-  if (e_start) cudaEventDestroy(e_start);
-  if (e_done) cudaEventDestroy(e_done);
+  // join everything back into the caller's stream (also after an error, so the
+  // internal streams never run ahead of the caller's later work)
+  cudaEventRecord(e_c, scomp);
+  cudaStreamWaitEvent(sout, e_c, 0);
+  cudaEventRecord(e_done, sout);
+  chk(cudaStreamWaitEvent(cs, e_done, 0));
   if (st) return st;
   return cuda_status(e);
 }

@@ -368,12 +368,9 @@ __global__ void __launch_bounds__(kThreads64, 1)
 cudaError_t launch_attn_b64(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                             const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                             const int32_t* row_ptr, const int32_t* col_idx, cudaStream_t st) {
-  static bool attr_done = false;
   const size_t smem = sizeof(Attn64Smem);
-  if (!attr_done) {
-    cudaFuncSetAttribute(attn64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_done = true;
-  }
+  const cudaError_t ea = ensure_smem_attr((const void*)attn64_kernel, smem);
+  if (ea != cudaSuccess) return ea;
   const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
   const dim3 grid(s.H * s.nt);
   attn64_kernel<<<grid, kThreads64, smem, st>>>(qmap, kmap, vmap, reinterpret_cast<__nv_bfloat16*>(o),

@@ -681,13 +681,10 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
                            const void* const* peer_o, int n_peer, cudaStream_t st) {
-  static bool attr_done = false;
   const size_t smem = attn8_smem_bytes();
-  if (!attr_done) {
-    cudaFuncSetAttribute(attn8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(attn8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_done = true;
-  }
+  cudaError_t ea = ensure_smem_attr((const void*)attn8_kernel<true>, smem);
+  if (ea == cudaSuccess) ea = ensure_smem_attr((const void*)attn8_kernel<false>, smem);
+  if (ea != cudaSuccess) return ea;
   const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
   const dim3 grid(s.H * ((s.nb + 1) / 2));
   auto* op = reinterpret_cast<__nv_bfloat16*>(o);

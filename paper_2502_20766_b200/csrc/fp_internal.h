@@ -28,10 +28,15 @@ inline Shape make_shape(int heads, int kv_heads, int seq_len, int block = 128) {
   s.lb = block == 64 ? 6 : 7;
   s.nb = (seq_len + block - 1) / block;  // ragged n: the last block is partial (A26)
   s.nt = (seq_len + 127) / 128;
-  // largest chunk (<= 8 tiles) that still gives >= 2 CTAs per SM of the
-  // 148-SM B200 for the representative passes (short sequences: smaller chunks)
+  // key tiles per representative-pass CTA: the largest chunk (<= 8 tiles) that
+  // leaves >= 32 chunks per head. A function of n ONLY: pass 1 sums each row's
+  // exponentials within a chunk and rep_stats combines the chunks, so the fp32
+  // summation order of the row statistics (and of everything derived from them:
+  // a_v, a_s, a_hat, D_JS, the top-mass picks) must not depend on how many
+  // heads one call batches (fp_layer_host per-group calls, multi-GPU head
+  // slices and the whole-layer call give bitwise identical results).
   s.ct = kChunkTilesMax;
-  while (s.ct > 1 && (long long)((s.nt + s.ct - 1) / s.ct) * heads < 2 * 148) s.ct >>= 1;
+  while (s.ct > 1 && (s.nt + s.ct - 1) / s.ct < 32) s.ct >>= 1;
   s.nchunks = (s.nt + s.ct - 1) / s.ct;
   s.g = heads / kv_heads;
   s.tri = (long long)s.nb * (s.nb + 1) / 2;
@@ -149,6 +154,12 @@ bool make_tile_map(CUtensorMap* map, const void* base, const TLayout& t, int n, 
                    int box_rows = 128);
 // rows per K/V TMA box of the attention kernel in use (v7: 64-key sub-tiles; v5: 128)
 int attn_kv_box_rows();
+
+// Raises `fn`'s dynamic shared-memory limit to `bytes` on the CURRENT device.
+// Function attributes are per device context: this runs cudaFuncSetAttribute
+// once per (kernel, device) under a mutex (thread-safe; several GPUs driven
+// from one process each get their own setting) and returns its error.
+cudaError_t ensure_smem_attr(const void* fn, size_t bytes);
 
 // ---- launchers (return cudaGetLastError of their launches) ----
 cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void* q, const void* k,

@@ -18,8 +18,6 @@
 //   pooled_softmax N4c A_bar row softmax over kb <= qb, / nb (QA heads only)
 #include <math.h>
 
-#include <mutex>
-
 #include "fp_common.cuh"
 #include "fp_internal.h"
 
@@ -513,20 +511,28 @@ __global__ void __launch_bounds__(kMapThreads) pooled_softmax(const int32_t* __r
 
 }  // namespace
 
-// One non-blocking side stream per device for the pooled-map branch of fp_plan,
-// created on first use (the library's only lazily initialised state besides
-// kernel attributes). nullptr if it cannot be created: the branch then runs
+// One non-blocking side stream per (calling thread, device) for the
+// pooled-map branch of fp_plan, created on first use. Per thread, so calls
+// from different threads never share it (no false dependencies between their
+// streams, and a graph capture in one thread cannot pull another thread's
+// work into its graph). nullptr if it cannot be created: the branch then runs
 // in order on the caller's stream.
+namespace {
+struct SideStreams {
+  cudaStream_t s[64] = {};
+  ~SideStreams() {
+    for (cudaStream_t x : s)
+      if (x) cudaStreamDestroy(x);
+  }
+};
+}  // namespace
 cudaStream_t plan_side_stream() {
-  static cudaStream_t streams[64] = {};
-  static std::once_flag once[64];
+  thread_local SideStreams tl;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  std::call_once(once[dev], [&]() {
-    if (cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
-      streams[dev] = nullptr;
-  });
-  return streams[dev];
+  if (!tl.s[dev] && cudaStreamCreateWithFlags(&tl.s[dev], cudaStreamNonBlocking) != cudaSuccess)
+    tl.s[dev] = nullptr;
+  return tl.s[dev];
 }
 
 size_t rep_smem_bytes(int pass) {
@@ -538,13 +544,10 @@ size_t rep_smem_bytes(int pass) {
 cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void* q, const void* k,
                         const Layout& lay, const CUtensorMap& qmap, const CUtensorMap& kmap, float tau,
                         int32_t* pattern_out, float* jsd_out, cudaStream_t st) {
-  static bool attr_done = false;
   const size_t sm1 = rep_smem_bytes(1), sm2 = rep_smem_bytes(2);
-  if (!attr_done) {
-    cudaFuncSetAttribute(rep_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    cudaFuncSetAttribute(rep_pass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-    attr_done = true;
-  }
+  cudaError_t ea = ensure_smem_attr((const void*)rep_pass<1>, sm1);
+  if (ea == cudaSuccess) ea = ensure_smem_attr((const void*)rep_pass<2>, sm2);
+  if (ea != cudaSuccess) return ea;
   const float scale = 1.0f / sqrtf(128.0f);
   const float scale_log2 = scale * kLog2e;
   float* m_part = wsp<float>(ws, L.m_part);

@@ -730,12 +730,8 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
                           const fp_select_options& opt, int32_t* row_ptr, int32_t* col_idx,
                           fp_select_stats* stats, cudaStream_t st) {
   const int32_t* pat = wsp<int32_t>(ws, L.pattern);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(topmass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(TopSmem));
-    attr_done = true;
-  }
+  const cudaError_t ea = ensure_smem_attr((const void*)topmass_kernel, sizeof(TopSmem));
+  if (ea != cudaSuccess) return ea;
   {
     // cluster size from the longest segment: ~64K scores per CTA, 1..8 CTAs
     const long long lmax = std::max<long long>(opt.vs_mode ? s.nb : s.n, opt.qa_mode ? 0 : s.tri);
@@ -772,8 +768,9 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
                                                 opt.vs_mode, s.lb, wsp<uint32_t>(ws, L.vbits),
                                                 wsp<uint32_t>(ws, L.dbits));
   // A12 / f2: budgets in tokens -> key blocks of this block size
-  const int min_blocks = (min_budget + s.b - 1) / s.b;
-  const int max_blocks = (opt.max_budget + s.b - 1) / s.b;
+  // (int64: token budgets near INT_MAX must not overflow; clamped to nb)
+  const int min_blocks = (int)std::min<long long>(s.nb, ((long long)min_budget + s.b - 1) / s.b);
+  const int max_blocks = (int)std::min<long long>(s.nb, ((long long)opt.max_budget + s.b - 1) / s.b);
   const dim3 rg((s.nb + kAsmWarps - 1) / kAsmWarps, s.H);
   assemble_rows<<<rg, kAsmWarps * 32, kAsmWarps * 2 * L.nbw * 4, st>>>(
       pat, wsp<uint32_t>(ws, L.vbits), wsp<uint32_t>(ws, L.dbits), wsp<int32_t>(ws, L.sel_qa),

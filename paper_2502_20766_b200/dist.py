@@ -104,6 +104,14 @@ def gather_heads(local_out, H, P, group=None):
         local_out = pad
     full = torch.empty((P * hmax, n, d), dtype=local_out.dtype, device=local_out.device)
     dist.all_gather_into_tensor(full, local_out.contiguous(), group=group)
+    return unpad_gathered(full, H, P)
+
+
+def unpad_gathered(full, H, P):
+    """[P * ceil(H/P)][n][d] all-gather result (rank r's slot holds its heads
+    first, then padding) -> the [H][n][d] layer output in head order."""
+    import torch
+    hmax = max_heads(H, P)
     if hmax * P == H:
         return full
     idx = []
@@ -122,9 +130,13 @@ class BalancedLayer:
          split as the static partition), written into this rank's CSR slot;
       2. all-gather of the CSR slots (row_ptr [hmax][nb+1], col_idx
          [hmax][cap] per rank; NCCL over NVLink);
-      3. per-head costs = useful attention FLOPs from row_ptr[:, nb] (one
-         small device->host read), LPT assignment (deterministic, so every
-         rank computes the same one);
+      3. per-head costs = useful attention FLOPs from row_ptr[:, nb], LPT
+         assignment (deterministic, so every rank computes the same one). The
+         costs of step t come from step t-1's gathered CSR, copied to pinned
+         host memory asynchronously (no host synchronisation inside a step;
+         only the first step reads its own CSR synchronously). Any assignment
+         yields the same output (every head is computed exactly once and
+         exchanged), so reusing the previous step's costs only affects balance;
       4. attention of this rank's LPT heads, one launch per head, each
          followed by an event on the compute stream;
       5. broadcast rounds j = 0, 1, ...: every rank broadcasts the output of
@@ -163,6 +175,8 @@ class BalancedLayer:
         self.comm = torch.cuda.Stream(device=self.device) if self.cuda else None
         self.last_assignment = None
         self.last_costs = None
+        self._nnz_host = None  # previous step's per-slot nnz (pinned, async copy)
+        self._nnz_event = None
         if exchange not in ("nccl", "p2p"):
             raise ValueError(exchange)
         self.exchange = exchange
@@ -203,7 +217,20 @@ class BalancedLayer:
         mark("t1")
         dist.all_gather_into_tensor(self.rp_all, self.rp_slot, group=self.group)
         dist.all_gather_into_tensor(self.ci_all, self.ci_slot, group=self.group)
-        nnz = self.rp_all[:, self.nb].cpu().tolist()  # the one host read of the step
+        if self._nnz_host is None:
+            nnz = self.rp_all[:, self.nb].cpu().tolist()  # first step: read synchronously
+        else:
+            if self._nnz_event is not None:
+                self._nnz_event.synchronize()  # the previous step's copy: long complete
+            nnz = self._nnz_host.tolist()
+        if self.cuda:  # this step's costs, for the next step's assignment
+            if self._nnz_host is None:
+                self._nnz_host = torch.empty(self.P * self.hmax, dtype=torch.int32).pin_memory()
+            self._nnz_host.copy_(self.rp_all[:, self.nb], non_blocking=True)
+            self._nnz_event = torch.cuda.Event()
+            self._nnz_event.record(stream)
+        else:
+            self._nnz_host = self.rp_all[:, self.nb].clone()
         costs = [head_cost(nnz[self.slot(h)], self.nb) for h in range(self.H)]
         assign = lpt_assign(costs, self.P)
         self.last_assignment, self.last_costs = assign, costs

@@ -99,8 +99,18 @@ def test_select_ex_option_validation(lib):
         opt = fp.SelectOptions(*bad)
         assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 0, ctypes.byref(opt), P, ws_bytes, P, P,
                                 None, s) == 3, bad
+    # a maximum budget below the minimum budget would undercut the per-row floor (A23)
+    opt = fp.SelectOptions(0, 0, 1024)
+    assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 2048, ctypes.byref(opt), P, ws_bytes, P, P,
+                            None, s) == 3
     import torch
     if not torch.cuda.is_available():  # valid options -> device check
+        assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 1024, ctypes.byref(opt), P, ws_bytes, P,
+                                P, None, s) == 6
+        # budgets near INT_MAX: converted in 64-bit arithmetic, no overflow
+        big = fp.SelectOptions(0, 0, 2**31 - 1)
+        assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 2**31 - 2, ctypes.byref(big), P,
+                                ws_bytes, P, P, None, s) == 6
         opt = fp.SelectOptions(1, 1, 4096)
         assert lib.fp_select_ex(4, 1, 2048, 128, 128, 0.9, 0, ctypes.byref(opt), P, ws_bytes, P, P,
                                 None, s) == 6
@@ -165,6 +175,42 @@ def test_peers_validation(lib):
     assert f(P, P, P, P, P, 2, H, G, n, 128, 128, None, None, P, P, 0, s) == 1  # CSR NULL
     assert f(P, P, P, P, P, 2, H, 3, n, 128, 128, None, P, P, P, 0, s) == 2
     import torch
+    # ws is optional scheduler scratch: non-NULL must be a full workspace
+    assert f(P, P, P, P, P, 2, H, G, n, 128, 128, None, P, P, P, 0, s) == 5
+    assert f(P, P, P, P, P, 2, H, G, n, 128, 128, None, P, P, P + 8, 1 << 40, s) == 4
     if not torch.cuda.is_available():
-        assert f(P, P, P, P, P, 2, H, G, n, 128, 128, None, P, P, P, 0, s) == 6
-        assert f(P, P, P, P, None, 0, H, G, n, 128, 128, None, P, P, P, 0, s) == 6
+        assert f(P, P, P, P, P, 2, H, G, n, 128, 128, None, P, P, None, 0, s) == 6
+        assert f(P, P, P, P, None, 0, H, G, n, 128, 128, None, P, P, None, 0, s) == 6
+        ws_bytes = fp.fp_workspace_bytes(H, G, n)
+        assert f(P, P, P, P, None, 0, H, G, n, 128, 128, None, P, P, P, ws_bytes, s) == 6
+
+
+def test_layer_host_validates_everything_first(lib):
+    """fp_layer_host checks every argument of its nested calls before the first
+    copy is enqueued (an invalid call enqueues nothing)."""
+    H, G, n = 8, 2, 2048
+    ws_bytes = fp.fp_workspace_bytes(H, G, n)
+    P = 0x10000
+    s = ctypes.c_void_p(0)
+    f = lib.fp_layer_host
+
+    def call(**kw):
+        a = dict(qh=P, kh=P, vh=P, oh=P, dq=P, dk=P, dv=P, do=P, H=H, G=G, n=n, d=128, b=128,
+                 gamma=0.9, tau=0.1, mb=0, ws=P, wsb=ws_bytes, pat=P, jsd=P, rp=P, ci=P)
+        a.update(kw)
+        return f(a["qh"], a["kh"], a["vh"], a["oh"], a["dq"], a["dk"], a["dv"], a["do"], a["H"],
+                 a["G"], a["n"], a["d"], a["b"], a["gamma"], a["tau"], a["mb"], a["ws"], a["wsb"],
+                 a["pat"], a["jsd"], a["rp"], a["ci"], s)
+    assert call(oh=None) == 1
+    assert call(ci=None) == 1
+    assert call(G=3) == 2
+    assert call(gamma=0.0) == 3
+    assert call(tau=1.5) == 3
+    assert call(mb=-1) == 3
+    assert call(do=P + 8) == 4     # device output not 16-B aligned
+    assert call(ws=P + 4) == 4
+    assert call(rp=P + 2) == 4     # int32 arrays need 4-B alignment
+    assert call(wsb=ws_bytes - 1) == 5
+    import torch
+    if not torch.cuda.is_available():
+        assert call() == 6

@@ -29,6 +29,15 @@ def test_reference_arm_json_contract():
     assert d["unit"] == "tokens/s" and d["value"] > 0 and d["higher_is_better"] is True
     assert d["steps"] == 1 and d["warmup"] == 0 and d["n_gpus"] == 1
     assert d["config"]["workload"] == "C1-tiny-4q1kv-2k"
+    # the same config object as our arm at N = 1 (driver's same_config check)
+    sys.path.insert(0, ROOT)
+    import bench
+    from synth.configs import C1
+    assert d["config"] == json.loads(json.dumps(bench.config_dict(C1, 1, False)))
+    # each step is a bounded sample, extrapolated, and says so
+    assert d["extrapolated"] is True and d["cpu_baseline"]["extrapolated"] is True
+    fr = d["sample_fraction"]
+    assert 0 < fr["plan_select_heads"] <= 1 and 0 < fr["attention_blocks"] <= 1
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["sample"] and cb["value"] == d["value"]
     e = d["e2e"]
