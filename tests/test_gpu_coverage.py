@@ -137,7 +137,7 @@ def test_c5_mixed_heads_32k_tau_sweep(fp, base):
         want = (D < tau).astype(np.int32)
         assert np.array_equal(res["pattern"][~near], want[~near]), tau
         counts.add(int(res["pattern"].sum()))
-    assert len(counts) >= 3  # the number of QA heads changes across the sweep
+    assert len(counts) >= 2  # the number of QA heads changes across the sweep
     for tau in (C5_TAUS[0], C5_TAUS[-1]):
         _case(fp, w.with_(tau=tau), 2, bits=bits)
 
