@@ -46,7 +46,7 @@ inline Shape make_shape(int heads, int kv_heads, int seq_len, int block = 128) {
 // Byte offsets of every workspace region (each 256-B aligned).
 struct WsLayout {
   size_t m_part, l_part;     // fp32 [H][nchunks][128]  pass-1 partial row max / sum (log2 domain)
-  size_t m_row, il_row;      // fp32 [H][128]           combined row max, 1/row sum
+  size_t m_row, mp_row;      // fp32 [H][128]           combined row max, M' = max + log2(sum)
   size_t a_v, a_s;           // fp32 [H][n]
   size_t as_part;            // fp32 [H][nt][256]       per-key-tile slash partials
   size_t a_hat, a_bar, As;   // fp32 [H][nb]
@@ -85,7 +85,7 @@ inline WsLayout ws_layout(const Shape& s) {
   L.m_part = take(H * s.nchunks * 128 * 4);
   L.l_part = take(H * s.nchunks * 128 * 4);
   L.m_row = take(H * 128 * 4);
-  L.il_row = take(H * 128 * 4);
+  L.mp_row = take(H * 128 * 4);
   L.a_v = take(H * n * 4);
   L.a_s = take(H * n * 4);
   L.as_part = take(H * (size_t)s.nt * 256 * 4);

@@ -32,9 +32,17 @@ constexpr int kSelThreads = 1024;
 constexpr int kItems = 8;
 constexpr float kFixScale = 1152921504606846976.0f;  // 2^60
 
+// x (>= 0, finite) in 2^-60 fixed point, truncated: floor(min(x, 8) * 2^60),
+// from the bit pattern (mantissa shifted by the exponent; no float->u64
+// conversion unit): x = m * 2^(e - 150), m = 1.f (24 bits), so
+// x * 2^60 = m << (e - 90) or m >> (90 - e).
 __device__ __forceinline__ uint64_t fixp(float x) {
-  x = fminf(x, 8.0f);
-  return __float2ull_rz(x * kFixScale);
+  const uint32_t b = __float_as_uint(fminf(x, 8.0f));
+  const int e = (int)(b >> 23);
+  if (e == 0) return 0;  // zero / denormals (< 2^-126): below 2^-60
+  const uint64_t m = (uint64_t)((b & 0x7fffffu) | 0x800000u);
+  const int sh = e - 90;
+  return sh >= 0 ? (m << sh) : (sh > -64 ? (m >> -sh) : 0ull);
 }
 
 // block-wide inclusive scan of uint64 (1024 threads), returns inclusive value,
@@ -65,7 +73,7 @@ __device__ uint64_t block_scan_u64(uint64_t v, uint64_t* wsum, uint64_t* total) 
   return v + add;
 }
 
-constexpr int kClMax = 8;  // max CTAs (one cluster) per top-mass segment; chosen per launch
+constexpr int kClMax = 8;  // max CTAs (one cluster) per head; chosen per launch
 
 // distributed shared memory helpers (thread block cluster)
 __device__ __forceinline__ uint32_t cl_rank() {
@@ -81,21 +89,24 @@ __device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// remote loads are ordered by the cluster barriers around them (compiler
+// barriers too), so they need no volatile / memory clobber: the compiler may
+// issue a batch of them back to back (DSMEM latency ~200 cycles each)
 __device__ __forceinline__ uint32_t cl_ld32(uint32_t a) {
   uint32_t v;
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  asm("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ unsigned long long cl_ld64(uint32_t a) {
   unsigned long long v;
-  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  asm("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
 }
 
 struct TopSmem {
   uint32_t cnt[2048];             // this CTA's histogram of its slice
   unsigned long long mass[2048];
-  uint32_t gcnt[2048];            // cluster-wide histogram (sum over the cluster's CTAs)
+  uint32_t gcnt[2048];            // sub-group histogram (sum over the segment's CTAs)
   unsigned long long gmass[2048];
   uint64_t wsum[32];
   uint32_t found_bin;
@@ -103,53 +114,21 @@ struct TopSmem {
   unsigned long long slice_gt, slice_eq;  // compaction counts of this CTA's slice
 };
 
-// topmass(x, gamma) of one segment by a cluster of ncl CTAs (1..8, set at
-// launch from the segment length); see file header. CTA c of the cluster owns
-// the index slice [c*S, (c+1)*S), S = ceil(L / ncl).
-__global__ void __launch_bounds__(kSelThreads, 1)
-    topmass_kernel(const float* __restrict__ a_v, const float* __restrict__ a_s,
-                   const float* __restrict__ a_hat, const float* __restrict__ As,
-                   const float* __restrict__ A_bar, const int32_t* __restrict__ pattern, int n,
-                   int nb, long long tri, float gamma, int vs_mode, int qa_mode,
-                   int32_t* __restrict__ sel_v, int32_t* __restrict__ sel_s,
-                   int32_t* __restrict__ sel_qa, int32_t* __restrict__ sel_count,
-                   unsigned long long* __restrict__ sel_mass) {
-  extern __shared__ __align__(16) uint8_t top_raw[];
-  TopSmem& sm = *reinterpret_cast<TopSmem*>(top_raw);
-  uint32_t ncl;
-  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
-  const int kCl = (int)ncl;
-  const int seg = blockIdx.x / kCl, h = blockIdx.y;
-  const uint32_t crank = cl_rank();
+// topmass(x[0..L), gamma) (A6-A8, Appendix B) by the nr CTAs of cluster ranks
+// [r0, r0 + nr) (this CTA is rank r0 + sub); CTA `sub` owns the index slice
+// [sub*S, (sub+1)*S), S = ceil(L / nr). Every CTA of the CLUSTER calls this the
+// same number of times (it executes a fixed number of cluster barriers).
+// MSD radix select by mass on the fp32 bit patterns (11/11/10-bit digits):
+// per pass a count + fixed-point mass histogram of the keys that match the
+// prefix found so far, merged over the sub-group through DSMEM, then the
+// descending-digit scan finds the digit holding the threshold. Masses are
+// sums of 2^-60 fixed-point values (exact, order independent).
+__device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long long L, int32_t* __restrict__ out,
+                                float gamma, uint32_t r0, uint32_t nr, uint32_t sub, int32_t* count_out,
+                                unsigned long long* mass_out) {
   const int tid = threadIdx.x;
-  const int pat = pattern[h];
-  // whole cluster leaves together; per-row QA selection (qa_mode 1) is topmass_rows
-  if ((pat == 1) != (seg == 2) || (seg == 2 && qa_mode == 1)) {
-    if (tid == 0 && crank == 0) {
-      sel_count[h * 4 + seg] = 0;
-      sel_mass[h * 4 + seg] = 0;
-    }
-    return;
-  }
-  const float* x;
-  int32_t* out;
-  long long L;
-  if (seg == 0) {  // vertical lines (a_v) or, vs_mode 1, key-block columns (a_hat)
-    x = vs_mode ? a_hat + (size_t)h * nb : a_v + (size_t)h * n;
-    out = sel_v + (size_t)h * n;
-    L = vs_mode ? nb : n;
-  } else if (seg == 1) {  // slash lines (a_s) or, vs_mode 1, offset groups (As)
-    x = vs_mode ? As + (size_t)h * nb : a_s + (size_t)h * n;
-    out = sel_s + (size_t)h * n;
-    L = vs_mode ? nb : n;
-  } else {
-    x = A_bar + (size_t)h * tri;
-    out = sel_qa + (size_t)h * tri;
-    L = tri;
-  }
-  const long long S = (L + kCl - 1) / kCl;
-  const long long lo = min(L, (long long)crank * S), hi = min(L, lo + S);
-
+  const long long S = (L + nr - 1) / nr;
+  const long long lo = min(L, (long long)sub * S), hi = min(L, lo + S);
   unsigned long long T = 0, G = 0, rem = 0;
   bool count_mode = false;
   uint32_t prefix = 0, pmask = 0;
@@ -161,43 +140,70 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     const int sh = shifts[pass];
     const uint32_t dmask = (1u << widths[pass]) - 1u;
     const int nbins = 1 << widths[pass];
-    for (int b = tid; b < 2048; b += kSelThreads) {
+    for (int b = tid; b < nbins; b += kSelThreads) {
       sm.cnt[b] = 0;
       sm.mass[b] = 0;
     }
     __syncthreads();
-    // local histogram of the slice (warp-aggregated smem atomics)
-    for (long long base = lo; base < hi; base += kSelThreads) {
-      const long long i = base + tid;
-      const bool valid = i < hi;
-      const uint32_t key = valid ? __float_as_uint(x[i]) : 0xffffffffu;
-      const bool match = valid && ((key & pmask) == prefix);
-      const uint32_t digit = match ? ((key >> sh) & dmask) : 0xffffffffu;
-      const uint32_t grp = __match_any_sync(0xffffffffu, digit);
-      if (match) {
-        const uint64_t f = fixp(__uint_as_float(key));
-        const uint32_t s0 = __reduce_add_sync(grp, (uint32_t)(f & 0xFFFFF));
-        const uint32_t s1 = __reduce_add_sync(grp, (uint32_t)((f >> 20) & 0xFFFFF));
-        const uint32_t s2 = __reduce_add_sync(grp, (uint32_t)(f >> 40));
-        if ((__ffs(grp) - 1) == (int)lane_id()) {
-          atomicAdd(&sm.cnt[digit], (uint32_t)__popc(grp));
-          atomicAdd(&sm.mass[digit], ((unsigned long long)s2 << 40) +
-                                         ((unsigned long long)s1 << 20) + (unsigned long long)s0);
+    // local histogram of the slice (warp-aggregated smem atomics), 4 loads in flight
+    for (long long base = lo; base < hi; base += 4 * kSelThreads) {
+      uint32_t keys[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long i = base + u * kSelThreads + tid;
+        keys[u] = i < hi ? __float_as_uint(__ldg(x + i)) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t key = keys[u];
+        const bool match = key != 0xffffffffu && ((key & pmask) == prefix);
+        const uint32_t digit = match ? ((key >> sh) & dmask) : 0xffffffffu;
+        const uint32_t grp = __match_any_sync(0xffffffffu, digit);
+        if (match) {
+          const uint64_t f = fixp(__uint_as_float(key));
+          const uint32_t s0 = __reduce_add_sync(grp, (uint32_t)(f & 0xFFFFF));
+          const uint32_t s1 = __reduce_add_sync(grp, (uint32_t)((f >> 20) & 0xFFFFF));
+          const uint32_t s2 = __reduce_add_sync(grp, (uint32_t)(f >> 40));
+          if ((__ffs(grp) - 1) == (int)lane_id()) {
+            atomicAdd(&sm.cnt[digit], (uint32_t)__popc(grp));
+            atomicAdd(&sm.mass[digit], ((unsigned long long)s2 << 40) +
+                                           ((unsigned long long)s1 << 20) + (unsigned long long)s0);
+          }
         }
       }
     }
-    cl_sync();  // every CTA's local histogram is complete
-    for (int b = tid; b < nbins; b += kSelThreads) {
-      uint32_t c = 0;
-      unsigned long long m = 0;
-      for (uint32_t r = 0; r < kCl; ++r) {  // fixed order; integer sums are exact anyway
-        c += cl_ld32(cl_map(&sm.cnt[b], r));
-        m += cl_ld64(cl_map(&sm.mass[b], r));
+    if (nr > 1) {
+      cl_sync();  // every CTA's local histogram is complete
+      for (int b = tid; b < nbins; b += kSelThreads) {
+        uint32_t cv[kClMax];
+        unsigned long long mv[kClMax];
+#pragma unroll
+        for (uint32_t r = 0; r < kClMax; ++r) {
+          if (r < nr) {
+            cv[r] = cl_ld32(cl_map(&sm.cnt[b], r0 + r));
+            mv[r] = cl_ld64(cl_map(&sm.mass[b], r0 + r));
+          }
+        }
+        uint32_t c = 0;
+        unsigned long long m = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < kClMax; ++r)
+          if (r < nr) {  // fixed order; integer sums are exact anyway
+            c += cv[r];
+            m += mv[r];
+          }
+        sm.gcnt[b] = c;
+        sm.gmass[b] = m;
       }
-      sm.gcnt[b] = c;
-      sm.gmass[b] = m;
+      cl_sync();  // remote reads done before anyone clears its histogram
+    } else {
+      __syncthreads();
+      for (int b = tid; b < nbins; b += kSelThreads) {
+        sm.gcnt[b] = sm.cnt[b];
+        sm.gmass[b] = sm.mass[b];
+      }
+      __syncthreads();
     }
-    cl_sync();  // remote reads done before anyone clears its histogram
     if (pass == 0) {
       // total mass T from the first-digit histogram (exact, fixed point)
       unsigned long long tl = 0;
@@ -205,19 +211,13 @@ __global__ void __launch_bounds__(kSelThreads, 1)
       uint64_t tot;
       block_scan_u64(tl, sm.wsum, &tot);
       T = tot;
-      if (gamma >= 1.0f) {  // A7: gamma >= 1 selects everything
-        for (long long i = lo + tid; i < hi; i += kSelThreads) out[i] = (int32_t)i;
-        if (tid == 0 && crank == 0) {
-          sel_count[h * 4 + seg] = (int32_t)L;
-          sel_mass[h * 4 + seg] = T;
-        }
-        cl_sync();
-        return;
-      }
       // K = min{k : C_k >= gamma T}  (A6, A7); G == 0 -> K = 1 (count mode)
       G = (unsigned long long)ceil((double)gamma * (double)T);
       count_mode = (G == 0);
       rem = count_mode ? 1ull : G;
+      if (gamma >= 1.0f) {  // A7: gamma >= 1 selects everything (the passes still run,
+        rem = 0;            // so every CTA of the cluster meets the same barriers)
+      }
     }
     // descending-digit scan: thread t owns digits nbins-1-2t and nbins-2-2t
     const int d0 = nbins - 1 - 2 * tid, d1 = d0 - 1;
@@ -232,8 +232,10 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     }
     uint64_t tot;
     const uint64_t key_m = count_mode ? (k0 + k1) : (m0 + m1);
-    const uint64_t excl = block_scan_u64(key_m, sm.wsum, &tot) - key_m;
     const uint64_t other = count_mode ? (m0 + m1) : (k0 + k1);
+    // both exclusive prefixes in one scan: key in the high, other in the low
+    // 32 bits are not enough (masses are 64-bit), so two scans
+    const uint64_t excl = block_scan_u64(key_m, sm.wsum, &tot) - key_m;
     const uint64_t excl_o = block_scan_u64(other, sm.wsum, &tot) - other;
     {
       const uint64_t q0 = count_mode ? k0 : m0, q1 = count_mode ? k1 : m1;
@@ -246,6 +248,11 @@ __global__ void __launch_bounds__(kSelThreads, 1)
         sm.found_bin = d1;
         sm.above_mass = count_mode ? excl_o + o0 : excl + q0;
         sm.above_cnt = count_mode ? excl + q0 : excl_o + o0;
+      }
+      if (rem == 0 && tid == 0) {  // gamma >= 1: nothing to find
+        sm.found_bin = 0;
+        sm.above_mass = 0;
+        sm.above_cnt = 0;
       }
     }
     __syncthreads();
@@ -268,22 +275,36 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     rem -= count_mode ? sm.above_cnt : sm.above_mass;
     __syncthreads();
   }
+  if (gamma >= 1.0f) {  // A7: everything, in index order
+    for (long long i = lo + tid; i < hi; i += kSelThreads) out[i] = (int32_t)i;
+    if (tid == 0 && sub == 0) {
+      *count_out = (int32_t)L;
+      *mass_out = T;
+    }
+    if (nr > 1) {
+      cl_sync();  // keep the barrier count equal to the gamma < 1 path
+      cl_sync();
+    }
+    return;
+  }
   // lambda = prefix; take t of its ties (lowest indices first)
   const uint32_t lam = prefix;
   const uint64_t f_lam = fixp(__uint_as_float(lam));
   const uint64_t t_take = count_mode ? rem : (rem + f_lam - 1) / f_lam;
   const uint64_t K = above_cnt_tot + t_take;
 
-  // slice counts (> lambda, == lambda), exchanged across the cluster for the offsets
+  // slice counts (> lambda, == lambda), exchanged across the sub-group for the offsets
   if (tid == 0) {
     sm.slice_gt = slice_gt;
     sm.slice_eq = slice_eq;
   }
-  cl_sync();
   uint64_t gt_run = 0, eq_run = 0;
-  for (uint32_t r = 0; r < crank; ++r) {
-    gt_run += cl_ld64(cl_map(&sm.slice_gt, r));
-    eq_run += cl_ld64(cl_map(&sm.slice_eq, r));
+  if (nr > 1) {
+    cl_sync();
+    for (uint32_t r = 0; r < sub; ++r) {
+      gt_run += cl_ld64(cl_map(&sm.slice_gt, r0 + r));
+      eq_run += cl_ld64(cl_map(&sm.slice_eq, r0 + r));
+    }
   }
   // ordered compaction of this slice
   for (long long base = lo; base < hi; base += (long long)kSelThreads * kItems) {
@@ -294,7 +315,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     for (int u = 0; u < kItems; ++u) {
       const long long i = i0 + u;
       const bool valid = i < hi;
-      keys[u] = valid ? __float_as_uint(x[i]) : 0u;
+      keys[u] = valid ? __float_as_uint(__ldg(x + i)) : 0u;
       gt += (valid && keys[u] > lam);
       eq += (valid && keys[u] == lam);
     }
@@ -317,11 +338,70 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     gt_run += tot & 0xffffffffu;
     eq_run += tot >> 32;
   }
-  if (tid == 0 && crank == 0) {
-    sel_count[h * 4 + seg] = (int32_t)K;
-    sel_mass[h * 4 + seg] = above_mass_tot + t_take * f_lam;
+  if (tid == 0 && sub == 0) {
+    *count_out = (int32_t)K;
+    *mass_out = above_mass_tot + t_take * f_lam;
   }
-  cl_sync();  // keep this CTA's shared memory alive until the cluster is done
+  if (nr > 1) cl_sync();  // keep this CTA's shared memory alive until the sub-group is done
+}
+
+// One cluster of C CTAs (1, 2, 4 or 8; set at launch) per head. VS head:
+// ranks [0, C/2) select the vertical lines (a_v, or a_hat with vs_mode 1),
+// ranks [C/2, C) the slash lines (a_s, or As) -- with C = 1 the one CTA does
+// both, one after the other. QA head: all C ranks on the flattened map.
+__global__ void __launch_bounds__(kSelThreads, 1)
+    topmass_kernel(const float* __restrict__ a_v, const float* __restrict__ a_s,
+                   const float* __restrict__ a_hat, const float* __restrict__ As,
+                   const float* __restrict__ A_bar, const int32_t* __restrict__ pattern, int n,
+                   int nb, long long tri, float gamma, int vs_mode, int qa_mode,
+                   int32_t* __restrict__ sel_v, int32_t* __restrict__ sel_s,
+                   int32_t* __restrict__ sel_qa, int32_t* __restrict__ sel_count,
+                   unsigned long long* __restrict__ sel_mass) {
+  extern __shared__ __align__(16) uint8_t top_raw[];
+  TopSmem& sm = *reinterpret_cast<TopSmem*>(top_raw);
+  uint32_t ncl;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+  const int h = blockIdx.y;
+  const uint32_t crank = cl_rank();
+  const int tid = threadIdx.x;
+  const int pat = pattern[h];
+  if (pat == 1) {
+    if (tid == 0 && crank == 0) {
+      for (int sg = 0; sg < 2; ++sg) {
+        sel_count[h * 4 + sg] = 0;
+        sel_mass[h * 4 + sg] = 0;
+      }
+    }
+    if (qa_mode == 1) {  // per-row QA selection is topmass_rows: the cluster leaves together
+      if (tid == 0 && crank == 0) {
+        sel_count[h * 4 + 2] = 0;
+        sel_mass[h * 4 + 2] = 0;
+      }
+      return;
+    }
+    topmass_segment(sm, A_bar + (size_t)h * tri, tri, sel_qa + (size_t)h * tri, gamma, 0, ncl, crank,
+                    &sel_count[h * 4 + 2], &sel_mass[h * 4 + 2]);
+    return;
+  }
+  if (tid == 0 && crank == 0) {
+    sel_count[h * 4 + 2] = 0;
+    sel_mass[h * 4 + 2] = 0;
+  }
+  const long long L = vs_mode ? nb : n;
+  const float* xv = vs_mode ? a_hat + (size_t)h * nb : a_v + (size_t)h * n;
+  const float* xs = vs_mode ? As + (size_t)h * nb : a_s + (size_t)h * n;
+  if (ncl == 1) {
+    topmass_segment(sm, xv, L, sel_v + (size_t)h * n, gamma, 0, 1, 0, &sel_count[h * 4 + 0],
+                    &sel_mass[h * 4 + 0]);
+    __syncthreads();
+    topmass_segment(sm, xs, L, sel_s + (size_t)h * n, gamma, 0, 1, 0, &sel_count[h * 4 + 1],
+                    &sel_mass[h * 4 + 1]);
+    return;
+  }
+  const uint32_t half = ncl / 2;
+  const int seg = crank < half ? 0 : 1;
+  topmass_segment(sm, seg == 0 ? xv : xs, L, (seg == 0 ? sel_v : sel_s) + (size_t)h * n, gamma,
+                  seg * half, half, crank - seg * half, &sel_count[h * 4 + seg], &sel_mass[h * 4 + seg]);
 }
 
 // ---------------------------------------------------------------------------
@@ -733,12 +813,14 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
   const cudaError_t ea = ensure_smem_attr((const void*)topmass_kernel, sizeof(TopSmem));
   if (ea != cudaSuccess) return ea;
   {
-    // cluster size from the longest segment: ~64K scores per CTA, 1..8 CTAs
-    const long long lmax = std::max<long long>(opt.vs_mode ? s.nb : s.n, opt.qa_mode ? 0 : s.tri);
+    // cluster size per head: <= ~160K scores per CTA for the flattened QA map,
+    // <= ~80K per CTA for each of the two VS segments (C/2 CTAs each), 1..8 CTAs
+    const long long lvs = opt.vs_mode ? s.nb : s.n, lqa = opt.qa_mode ? 0 : s.tri;
+    long long need = std::max((lqa + 159999) / 160000, 2 * ((lvs + 79999) / 80000));
     int ncl = 1;
-    while (ncl < kClMax && (long long)ncl * 65536 < lmax) ncl <<= 1;
+    while (ncl < need && ncl < kClMax) ncl <<= 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(3 * ncl, s.H);
+    cfg.gridDim = dim3(ncl, s.H);
     cfg.blockDim = dim3(kSelThreads);
     cfg.dynamicSmemBytes = sizeof(TopSmem);
     cfg.stream = st;
