@@ -38,6 +38,8 @@
 // intra-block causal mask. When nb is odd the last pair has no row B.
 #include <math.h>
 
+#include <algorithm>
+
 #include "fp_common.cuh"
 #include "fp_internal.h"
 
@@ -91,7 +93,9 @@ struct Attn8Smem {
   uint8_t q[2][kTileBytes];  // Q_A, Q_B (1024-B aligned: first member)
   uint8_t k[kKS8][kTileBytes];
   uint8_t v[kVS8][kTileBytes];
-  uint64_t q_full;
+  uint64_t q_full, q_empty;
+  uint64_t item_full[2], item_empty[2];  // work-item id ring (persistent scheduling)
+  int item[2];
   uint64_t k_full[kKS8], k_empty[kKS8];
   uint64_t v_full[kVS8], v_empty[kVS8];
   uint64_t s_full[2], p_full[2], p_lo[2], pv_done[2];
@@ -251,65 +255,105 @@ FP_DEV void umma_pv_chain4(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc,
 #define COMMIT8(b) (kWarpIssue8 ? umma_commit_w(b) : umma_commit(b))
 
 // Merge of the two rows' sorted key-block lists: next union entry.
-// mask bit 0: row A selected it, bit 1: row B.
+// mask bit 0: row A selected it, bit 1: row B. The list heads are loaded one
+// entry ahead, so the global-load latency overlaps the caller's work.
 struct UnionIter {
   const int32_t* la;
   const int32_t* lb;
   int na, nb_, ia, ib;
   bool dense;
+  int ca, cb;  // key blocks at ia / ib (INT_MAX past the end)
+  FP_DEV void init(const int32_t* a_, const int32_t* b_, int na_, int nb2, bool d) {
+    la = a_;
+    lb = b_;
+    na = na_;
+    nb_ = nb2;
+    ia = ib = 0;
+    dense = d;
+    ca = na > 0 ? (dense ? 0 : __ldg(la)) : 0x7fffffff;
+    cb = nb_ > 0 ? (dense ? 0 : __ldg(lb)) : 0x7fffffff;
+  }
   FP_DEV bool done() const { return ia >= na && ib >= nb_; }
   FP_DEV int next(int& mask) {
-    const int ka = ia < na ? (dense ? ia : __ldg(la + ia)) : 0x7fffffff;
-    const int kb = ib < nb_ ? (dense ? ib : __ldg(lb + ib)) : 0x7fffffff;
-    const int k = min(ka, kb);
-    mask = (ka == k ? 1 : 0) | (kb == k ? 2 : 0);
-    ia += mask & 1;
-    ib += mask >> 1;
+    const int k = min(ca, cb);
+    mask = (ca == k ? 1 : 0) | (cb == k ? 2 : 0);
+    if (mask & 1) {
+      ++ia;
+      ca = ia < na ? (dense ? ia : __ldg(la + ia)) : 0x7fffffff;
+    }
+    if (mask & 2) {
+      ++ib;
+      cb = ib < nb_ ? (dense ? ib : __ldg(lb + ib)) : 0x7fffffff;
+    }
     return k;
   }
 };
 
+// One work item = (head h, q-block pair (qbA, qbB = qbA - 1)); items are
+// numbered KV-group-major, pairs descending, heads of a group interleaved (the
+// K/V of one group, 64 MiB at 128k, stay in L2 while its items run).
+struct Item {
+  int h, g, qbA, qbB, nA, nB;
+  const int32_t* la;
+  const int32_t* lb;
+};
+template <bool DENSE>
+FP_DEV Item decode_item(int item, int H, int G, int nb, long long cap, const int32_t* row_ptr,
+                        const int32_t* col_idx) {
+  Item it;
+  const int gsz = H / G;
+  const int npair = (nb + 1) >> 1;
+  const int per_group = gsz * npair;
+  it.g = item / per_group;
+  const int rem = item - it.g * per_group;
+  it.qbA = nb - 1 - 2 * (rem / gsz);
+  it.qbB = it.qbA - 1;  // -1: no row B
+  it.h = it.g * gsz + rem % gsz;
+  it.la = it.lb = nullptr;
+  if (DENSE) {
+    it.nA = it.qbA + 1;
+    it.nB = it.qbB + 1;
+  } else {
+    const int32_t* rp = row_ptr + (size_t)it.h * (nb + 1);
+    const int bA = __ldg(rp + it.qbA);
+    it.nA = __ldg(rp + it.qbA + 1) - bA;
+    it.la = col_idx + (size_t)it.h * cap + bA;
+    if (it.qbB >= 0) {
+      const int bB = __ldg(rp + it.qbB);
+      it.nB = bA - bB;
+      it.lb = col_idx + (size_t)it.h * cap + bB;
+    } else {
+      it.nB = 0;
+    }
+  }
+  return it;
+}
+
+// Persistent: gridDim.x <= #SMs CTAs (one per SM), each runs work items until
+// the list is exhausted. Items come from an atomic counter in the workspace
+// (work_counter, zeroed before the launch: dynamic balancing, the next item
+// goes to the first free SM). Without a workspace the grid has one CTA per
+// item (item = blockIdx.x). Warp 8 fetches the ids and publishes them through a 2-slot
+// ring (item_full / item_empty); every barrier phase below is counted
+// cumulatively over the CTA's items. Across items: the next item's Q tiles
+// are loaded once the last S MMA of the current one completed (q_empty), its
+// first S MMAs run while the softmax warpgroups finish the current item, and
+// a row's O is overwritten (first PV, accumulate = 0) only after its P -- which
+// the warpgroup produces after its previous epilogue read O -- is stored.
 template <bool DENSE>
 __global__ void __launch_bounds__(kThreads8, 1)
     attn8_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                  const __grid_constant__ CUtensorMap vmap, __nv_bfloat16* __restrict__ o,
                  const TLayout ol, int Hp, int Gp, int H, int G, int n, int nb, long long cap,
                  const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                 float scale_log2, const unsigned long long* __restrict__ peer_o, int n_peer) {
+                 float scale_log2, const unsigned long long* __restrict__ peer_o, int n_peer,
+                 int total_items, int* __restrict__ work_counter) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 tiles need 1024-B alignment
   Attn8Smem& sm = *reinterpret_cast<Attn8Smem*>(smem_raw);
 
   const int tid = threadIdx.x;
   const int wid = warp_id();
-  // work item (KV-group-major, q-block pairs descending, heads of the group interleaved)
-  const int gsz = H / G;
-  const int npair = (nb + 1) >> 1;
-  const int per_group = gsz * npair;
-  const int g = blockIdx.x / per_group;
-  const int rem = blockIdx.x - g * per_group;
-  const int qbA = nb - 1 - 2 * (rem / gsz);
-  const int qbB = qbA - 1;  // -1: no row B
-  const int h = g * gsz + rem % gsz;
-  int nA, nB;
-  const int32_t* la = nullptr;
-  const int32_t* lb = nullptr;
-  if (DENSE) {
-    nA = qbA + 1;
-    nB = qbB + 1;
-  } else {
-    const int32_t* rp = row_ptr + (size_t)h * (nb + 1);
-    const int bA = rp[qbA];
-    nA = rp[qbA + 1] - bA;
-    la = col_idx + (size_t)h * cap + bA;
-    if (qbB >= 0) {
-      const int bB = rp[qbB];
-      nB = bA - bB;
-      lb = col_idx + (size_t)h * cap + bB;
-    } else {
-      nB = 0;
-    }
-  }
 
   if (wid == 9) tmem_alloc(&sm.tmem_base, 512);
   if (tid == 256) {
@@ -317,6 +361,11 @@ __global__ void __launch_bounds__(kThreads8, 1)
     tma_prefetch_desc(&kmap);
     tma_prefetch_desc(&vmap);
     mbar_init(&sm.q_full, 1);
+    mbar_init(&sm.q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.item_full[i], 1);
+      mbar_init(&sm.item_empty[i], 10);  // V producer, issuer, 8 softmax warps
+    }
     for (int s = 0; s < kKS8; ++s) {
       mbar_init(&sm.k_full[s], 1);
       mbar_init(&sm.k_empty[s], 1);
@@ -337,6 +386,11 @@ __global__ void __launch_bounds__(kThreads8, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = sm.tmem_base;
+  // consumers: the k-th item id of this CTA (-1: no more work)
+  auto get_item = [&](int k) {
+    mbar_wait(&sm.item_full[k & 1], (k >> 1) & 1);
+    return sm.item[k & 1];
+  };
 
   if (wid >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
@@ -345,24 +399,43 @@ __global__ void __launch_bounds__(kThreads8, 1)
       if (lane_id() == 0) {
         const bool isK = (wid == 8);
         const uint64_t pol = policy_evict_last();
-        if (isK) {
-          mbar_arrive_expect_tx(&sm.q_full, nB > 0 ? 2 * kTileBytes : kTileBytes);
-          tma_tile(sm.q[0], &qmap, &sm.q_full, qbA * 128, h, Hp);
-          if (nB > 0) tma_tile(sm.q[1], &qmap, &sm.q_full, qbB * 128, h, Hp);
-        }
         const int depth = isK ? kKS8 : kVS8;
         uint64_t* full = isK ? sm.k_full : sm.v_full;
         uint64_t* empty = isK ? sm.k_empty : sm.v_empty;
         const CUtensorMap* map = isK ? &kmap : &vmap;
-        UnionIter it{la, lb, nA, nB, 0, 0, DENSE};
-        int e = 0;
-        for (; !it.done(); ++e) {
-          int mask;
-          const int kb = it.next(mask);
-          const int s = e % depth;
-          if (e >= depth) mbar_wait(&empty[s], ((e - depth) / depth) & 1);
-          mbar_arrive_expect_tx(&full[s], kTileBytes);
-          tma_tile_hint(isK ? sm.k[s] : sm.v[s], map, &full[s], kb * 128, g, Gp, pol);
+        int e = 0;  // union entries loaded so far (all items)
+        for (int k = 0;; ++k) {
+          int item;
+          if (isK) {
+            // scheduler: fetch the k-th item and publish it
+            item = work_counter ? atomicAdd(work_counter, 1) : (int)blockIdx.x + k * (int)gridDim.x;
+            if (item >= total_items) item = -1;
+            if (k >= 2) mbar_wait(&sm.item_empty[k & 1], ((k - 2) >> 1) & 1);
+            sm.item[k & 1] = item;
+            mbar_arrive(&sm.item_full[k & 1]);
+          } else {
+            item = get_item(k);
+            mbar_arrive(&sm.item_empty[k & 1]);
+          }
+          if (item < 0) break;
+          const Item it = decode_item<DENSE>(item, H, G, nb, cap, row_ptr, col_idx);
+          if (isK) {
+            // Q_A, Q_B of this item once the previous item's S MMAs are done
+            if (k >= 1) mbar_wait(&sm.q_empty, (k - 1) & 1);
+            mbar_arrive_expect_tx(&sm.q_full, it.nB > 0 ? 2 * kTileBytes : kTileBytes);
+            tma_tile(sm.q[0], &qmap, &sm.q_full, it.qbA * 128, it.h, Hp);
+            if (it.nB > 0) tma_tile(sm.q[1], &qmap, &sm.q_full, it.qbB * 128, it.h, Hp);
+          }
+          UnionIter un;
+          un.init(it.la, it.lb, it.nA, it.nB, DENSE);
+          for (; !un.done(); ++e) {
+            int mask;
+            const int kb = un.next(mask);
+            const int s = e % depth;
+            if (e >= depth) mbar_wait(&empty[s], ((e - depth) / depth) & 1);
+            mbar_arrive_expect_tx(&full[s], kTileBytes);
+            tma_tile_hint(isK ? sm.k[s] : sm.v[s], map, &full[s], kb * 128, it.g, Gp, pol);
+          }
         }
         // drain: the issuer releases every slot it consumes (it does not know
         // the union length); consume those releases before the CTA exits
@@ -374,77 +447,84 @@ __global__ void __launch_bounds__(kThreads8, 1)
         constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false);
         constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, true);
         const uint64_t qdesc[2] = {sdesc_kmajor(smem_u32(sm.q[0]), 0), sdesc_kmajor(smem_u32(sm.q[1]), 0)};
-        int pend[2] = {-1, -1};  // union entry of X's S awaiting its PV
-        int cnt[2] = {0, 0};     // S tiles issued per stream
+        int cnt[2] = {0, 0};     // S tiles issued per stream (all items)
+        int e = 0;               // union entries consumed (all items)
         FP_T8_DECL(lane_id() == 0);
-        auto issue_pv = [&](int x) {
-          const int e = pend[x];
-          const int vs = e % kVS8;
-          FP_T8(12);
-          mbar_wait(&sm.v_full[vs], (e / kVS8) & 1);
-          FP_T8(9);
-          const uint64_t vdesc = sdesc_mnmajor(smem_u32(sm.v[vs]), 0);
-          if (kSplit8) {
-            mbar_wait(&sm.p_lo[x], (cnt[x] - 1) & 1);
-            FP_T8(10);
-            tc_fence_after();
-#if !defined(FP_XMMA8) && !defined(FP_XPV8)
-            PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
-                           cnt[x] > 1);
-#endif
+        for (int k = 0;; ++k) {
+          const int item = get_item(k);
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
+          if (item < 0) break;
+          const Item itm = decode_item<DENSE>(item, H, G, nb, cap, row_ptr, col_idx);
+          int pend[2] = {-1, -1};  // union entry of X's S awaiting its PV
+          int lcnt[2] = {0, 0};    // S tiles issued per stream in this item
+          auto issue_pv = [&](int x) {
+            const int ep = pend[x];
+            const int vs = ep % kVS8;
             FP_T8(12);
-            mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
-            FP_T8(11);
-            tc_fence_after();
-#if !defined(FP_XMMA8) && !defined(FP_XPV8)
-            PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512,
-                           idesc_o, 1);
-#endif
-          } else {
-            mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
-            tc_fence_after();
-            umma_pv_chain8(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
-                           cnt[x] > 1);
-          }
-          COMMIT8(&sm.v_empty[vs]);
-          COMMIT8(&sm.pv_done[x]);
-          pend[x] = -1;
-        };
-        mbar_wait(&sm.q_full, 0);
-        UnionIter it{la, lb, nA, nB, 0, 0, DENSE};
-        for (int e = 0; !it.done(); ++e) {
-          int mask;
-          it.next(mask);
-          const int ks = e % kKS8;
-          FP_T8(12);
-          mbar_wait(&sm.k_full[ks], (e / kKS8) & 1);
-          FP_T8(8);
-#ifdef FP_TIMING
-          ++tacc[14];
-#endif
-          tc_fence_after();
-          const uint64_t kdesc = sdesc_kmajor(smem_u32(sm.k[ks]), 0);
-#pragma unroll
-          for (int x = 0; x < 2; ++x) {
-            if (pend[x] >= 0) issue_pv(x);
-            if (mask & (1 << x)) {
+            mbar_wait(&sm.v_full[vs], (ep / kVS8) & 1);
+            FP_T8(9);
+            const uint64_t vdesc = sdesc_mnmajor(smem_u32(sm.v[vs]), 0);
+            if (kSplit8) {
+              mbar_wait(&sm.p_lo[x], (cnt[x] - 1) & 1);
+              FP_T8(10);
+              tc_fence_after();
+              PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o, lcnt[x] > 1);
               FP_T8(12);
-#if !defined(FP_XMMA8) && !defined(FP_XS8)
-              SSCHAIN8(tbase + kColS8 + x * 128, qdesc[x], kdesc, idesc_s);
-#endif
-              FP_T8(13);  // issue time of the 8 S MMAs
-              COMMIT8(&sm.s_full[x]);
-              pend[x] = e;
-              ++cnt[x];
+              mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
+              FP_T8(11);
+              tc_fence_after();
+              PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512, idesc_o, 1);
+            } else {
+              mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
+              tc_fence_after();
+              umma_pv_chain8(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
+                             lcnt[x] > 1);
             }
+            COMMIT8(&sm.v_empty[vs]);
+            COMMIT8(&sm.pv_done[x]);
+            pend[x] = -1;
+          };
+          mbar_wait(&sm.q_full, k & 1);
+          UnionIter un;
+          un.init(itm.la, itm.lb, itm.nA, itm.nB, DENSE);
+          for (; !un.done(); ++e) {
+            int mask;
+            un.next(mask);
+            const int ks = e % kKS8;
+            FP_T8(12);
+            mbar_wait(&sm.k_full[ks], (e / kKS8) & 1);
+            FP_T8(8);
+#ifdef FP_TIMING
+            ++tacc[14];
+#endif
+            tc_fence_after();
+            const uint64_t kdesc = sdesc_kmajor(smem_u32(sm.k[ks]), 0);
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+              if (pend[x] >= 0) issue_pv(x);
+              if (mask & (1 << x)) {
+                FP_T8(12);
+#if !defined(FP_XMMA8) && !defined(FP_XS8)
+                SSCHAIN8(tbase + kColS8 + x * 128, qdesc[x], kdesc, idesc_s);
+#endif
+                FP_T8(13);  // issue time of the 8 S MMAs
+                COMMIT8(&sm.s_full[x]);
+                pend[x] = e;
+                ++cnt[x];
+                ++lcnt[x];
+              }
+            }
+            COMMIT8(&sm.k_empty[ks]);
+            // an entry only one row uses gets its second V-slot release here
+            // (it arrives early, but the phase also needs the PV's commit)
+            if (mask != 3) COMMIT8(&sm.v_empty[e % kVS8]);
           }
-          COMMIT8(&sm.k_empty[ks]);
-          // an entry only one row uses gets its second V-slot release here
-          // (it arrives early, but the phase also needs the PV's commit)
-          if (mask != 3) COMMIT8(&sm.v_empty[e % kVS8]);
+          // every S MMA of this item is issued: Q may be reloaded once they complete
+          COMMIT8(&sm.q_empty);
+          if (pend[0] >= 0) issue_pv(0);
+          if (pend[1] >= 0) issue_pv(1);
         }
-        if (pend[0] >= 0) issue_pv(0);
-        if (pend[1] >= 0) issue_pv(1);
         FP_T8(12);
         FP_T8_FLUSH(8, 15);
       }
@@ -453,78 +533,83 @@ __global__ void __launch_bounds__(kThreads8, 1)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     // ------------------------------------------------ softmax warpgroups
     const int x = wid >> 2;                     // 0 = row A, 1 = row B
-    const int nX = x ? nB : nA;
-    const int qb = x ? qbB : qbA;
     const int r = (wid & 3) * 32 + lane_id();   // query row within the block = TMEM lane
     const uint32_t lane_off = (uint32_t)((wid & 3) * 32) << 16;
     const uint32_t tS = tbase + kColS8 + x * 128 + lane_off;
     const uint32_t tO = tbase + kColO8 + x * 128 + lane_off;
-    float m_used = -INFINITY, l = 0.f;
+    int T = 0;  // tiles of this row processed in earlier items (barrier phases)
     FP_T8_DECL((wid & 3) == 0 && lane_id() == 0);
-    for (int t = 0; t < nX; ++t) {
-      FP_T8(6);
-      mbar_wait(&sm.s_full[x], t & 1);
-      FP_T8(0);
-#ifdef FP_XSM8
-      // experiment: softmax does no work (measures the MMA/issuer pipeline alone)
-      tc_fence_after();
+    for (int k = 0;; ++k) {
+      const int item = get_item(k);
       __syncwarp();
-      if (lane_id() == 0) { mbar_arrive(&sm.p_lo[x]); mbar_arrive(&sm.p_full[x]); }
-      continue;
+      if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
+      if (item < 0) break;
+      const Item itm = decode_item<DENSE>(item, H, G, nb, cap, row_ptr, col_idx);
+      const int nX = x ? itm.nB : itm.nA;
+      const int qb = x ? itm.qbB : itm.qbA;
+      float m_used = -INFINITY, l = 0.f;
+      for (int t = 0; t < nX; ++t) {
+        const int ph = (T + t) & 1;  // this tile's phase of s_full / p_lo / p_full
+        FP_T8(6);
+        mbar_wait(&sm.s_full[x], ph);
+        FP_T8(0);
+#ifdef FP_XSM8
+        // experiment: softmax does no work (measures the MMA/issuer pipeline alone)
+        tc_fence_after();
+        __syncwarp();
+        if (lane_id() == 0) { mbar_arrive(&sm.p_lo[x]); mbar_arrive(&sm.p_full[x]); }
+        continue;
 #endif
-      tc_fence_after();
-      float v[128];
-      tmem_ld_32x32b_x64_8(tS, reinterpret_cast<uint32_t*>(v));
-      tmem_ld_32x32b_x64_8(tS + 64, reinterpret_cast<uint32_t*>(v + 64));
-      // probe pv_done(t - 1) now (complete: S(t) followed PV(t - 1) in the
-      // in-order MMA stream) so the probe's latency overlaps the TMEM load;
-      // the phase is still consumed below, the loop only runs if it failed
-      const bool pv_ok = t == 0 || mbar_try_wait(smem_u32(&sm.pv_done[x]), (t - 1) & 1);
-      tmem_wait_ld();
-      FP_T8(1);
-      if (t == nX - 1) {  // the diagonal block: keys j <= r only
+        tc_fence_after();
+        float v[128];
+        tmem_ld_32x32b_x64_8(tS, reinterpret_cast<uint32_t*>(v));
+        tmem_ld_32x32b_x64_8(tS + 64, reinterpret_cast<uint32_t*>(v + 64));
+        // probe pv_done(t - 1) now (complete: S(t) followed PV(t - 1) in the
+        // in-order MMA stream) so the probe's latency overlaps the TMEM load;
+        // the phase is still consumed below, the loop only runs if it failed
+        const bool pv_ok = t == 0 || mbar_try_wait(smem_u32(&sm.pv_done[x]), (T + t - 1) & 1);
+        tmem_wait_ld();
+        FP_T8(1);
+        if (t == nX - 1) {  // the diagonal block: keys j <= r only
 #pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c > r) v[c] = -INFINITY;
-      }
-      // row max: 8 independent fmax3 chains (8 x 16 columns), then a tree
-      float mc[8];
+          for (int c = 0; c < 128; ++c)
+            if (c > r) v[c] = -INFINITY;
+        }
+        // row max: 8 independent fmax3 chains (8 x 16 columns), then a tree
+        float mc[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(v[16 * j], v[16 * j + 1], v[16 * j + 2]);
+        for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(v[16 * j], v[16 * j + 1], v[16 * j + 2]);
 #pragma unroll
-      for (int c = 3; c < 15; c += 2)
+        for (int c = 3; c < 15; c += 2)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(mc[j], v[16 * j + c], v[16 * j + c + 1]);
+          for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(mc[j], v[16 * j + c], v[16 * j + c + 1]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mc[j] = fmaxf(mc[j], v[16 * j + 15]);
-      const float mx = fmaxf(fmax3_8(mc[0], mc[1], mc[2]), fmax3_8(mc[3], mc[4], fmax3_8(mc[5], mc[6], mc[7]))) *
-                       scale_log2;
-      float alpha = 1.f;
-      if (mx > m_used + kRescale8) {
-        alpha = exp2f(m_used - mx);  // 0 on the first tile
-        m_used = mx;
-      }
-      const float nm = -m_used;
-      FP_T8(2);
-      if (kSplit8) {
+        for (int j = 0; j < 8; ++j) mc[j] = fmaxf(mc[j], v[16 * j + 15]);
+        const float mx = fmaxf(fmax3_8(mc[0], mc[1], mc[2]), fmax3_8(mc[3], mc[4], fmax3_8(mc[5], mc[6], mc[7]))) *
+                         scale_log2;
+        float alpha = 1.f;
+        if (mx > m_used + kRescale8) {
+          alpha = exp2f(m_used - mx);  // 0 on the first tile
+          m_used = mx;
+        }
+        const float nm = -m_used;
+        FP_T8(2);
         // O_X holds sum_{earlier} P V: PV of the previous tile completed before
         // S of this one (one in-order tcgen05.mma stream), so O can be
-        // rescaled now, before PV's first half is released
-        // every pv_done phase is consumed (here, normally long complete; an
-        // unconsumed phase is what compute-sanitizer synccheck reports)
-        if (!pv_ok) mbar_wait(&sm.pv_done[x], (t - 1) & 1);
+        // rescaled now, before PV's first half is released. Every pv_done
+        // phase is consumed (here, normally long complete; an unconsumed phase
+        // is what compute-sanitizer synccheck reports).
+        if (!pv_ok) mbar_wait(&sm.pv_done[x], (T + t - 1) & 1);
         if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-          {
-            tc_fence_after();
+          tc_fence_after();
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              uint32_t ov[32];
-              tmem_ld32(tO + q4 * 32, ov);
-              tmem_wait_ld();
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t ov[32];
+            tmem_ld32(tO + q4 * 32, ov);
+            tmem_wait_ld();
 #pragma unroll
-              for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
-              tmem_st32(tO + q4 * 32, ov);
-            }
+            for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
+            tmem_st32(tO + q4 * 32, ov);
           }
         }
         FP_T8(3);
@@ -573,89 +658,48 @@ __global__ void __launch_bounds__(kThreads8, 1)
 #ifdef FP_TIMING
         ++tacc[15];
 #endif
-        continue;
       }
+      if (nX > 0) {
+        // epilogue: O / l -> bf16 -> global (rows past n are not stored)
+        mbar_wait(&sm.pv_done[x], (T + nX - 1) & 1);
+        tc_fence_after();
+        const float il = 1.0f / l;
+        const int row = qb * 128 + r;
+        const size_t off = toff(ol, itm.h, row);
+        uint4* dst = reinterpret_cast<uint4*>(o + off);
 #pragma unroll
-      for (int c = 0; c < 128; c += 2) ffma2_8(v[c], v[c + 1], v[c], v[c + 1], scale_log2, nm);
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t ov[32];
+          tmem_ld32(tO + c0, ov);
+          tmem_wait_ld();
+          if (row < n) {
+            uint4 w4[4];
 #pragma unroll
-      for (int c = 0; c < 128 - kEmu8; ++c) v[c] = fast_exp2(v[c]);
+            for (int c = 0; c < 32; c += 8) {
+              uint32_t w[4];
 #pragma unroll
-      for (int c = 128 - kEmu8; c < 128; c += 2) exp2_emu2_8(v[c], v[c + 1], v[c], v[c + 1]);
-      if (kEmu8 > 0 && t == nX - 1) {
+              for (int e = 0; e < 4; ++e)
+                w[e] = pack_bf16x2(__uint_as_float(ov[c + 2 * e]) * il, __uint_as_float(ov[c + 2 * e + 1]) * il);
+              w4[c / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+              dst[(c0 + c) / 8] = w4[c / 8];
+            }
+            // next row f4: the same row into every peer's output buffer (another
+            // rank's buffer mapped into this process: the stores go over NVLink)
+            for (int i = 0; i < n_peer; ++i) {
+              uint4* pd = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(__ldg(peer_o + i)) + off);
 #pragma unroll
-        for (int c = 128 - kEmu8; c < 128; ++c)
-          if (c > r) v[c] = 0.f;
-      }
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-      for (int c = 0; c < 128; c += 4) {
-        fadd2_8(s0, s1, s0, s1, v[c], v[c + 1]);
-        fadd2_8(s2, s3, s2, s3, v[c + 2], v[c + 3]);
-      }
-      l = l * alpha + ((s0 + s1) + (s2 + s3));
-      uint32_t pk[64];
-#pragma unroll
-      for (int c = 0; c < 64; ++c) pk[c] = pack_bf16x2(v[2 * c], v[2 * c + 1]);
-      // O_X holds sum_{earlier} P V once PV of the previous tile is done
-      if (t > 0) {
-        mbar_wait(&sm.pv_done[x], (t - 1) & 1);
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
-          tc_fence_after();
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            uint32_t ov[32];
-            tmem_ld32(tO + q4 * 32, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
-            tmem_st32(tO + q4 * 32, ov);
+              for (int c = 0; c < 4; ++c) pd[c0 / 8 + c] = w4[c];
+            }
           }
         }
+        tc_fence_before();  // O reads complete before P of the next item is released
       }
-      tmem_st_32x32b_x64_8(tS, pk);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&sm.p_full[x]);
+      T += nX;
     }
     FP_T8_FLUSH(0, 8);
 #ifdef FP_TIMING
     if (t_on) atomicAdd(&g_attn8_timing[15], (unsigned long long)tacc[15]);
 #endif
-    if (nX > 0) {
-      // epilogue: O / l -> bf16 -> global (rows past n are not stored)
-      mbar_wait(&sm.pv_done[x], (nX - 1) & 1);
-      tc_fence_after();
-      const float il = 1.0f / l;
-      const int row = qb * 128 + r;
-      const size_t off = toff(ol, h, row);
-      uint4* dst = reinterpret_cast<uint4*>(o + off);
-#pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        uint32_t ov[32];
-        tmem_ld32(tO + c0, ov);
-        tmem_wait_ld();
-        if (row < n) {
-          uint4 w4[4];
-#pragma unroll
-          for (int c = 0; c < 32; c += 8) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              w[e] = pack_bf16x2(__uint_as_float(ov[c + 2 * e]) * il, __uint_as_float(ov[c + 2 * e + 1]) * il);
-            w4[c / 8] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[(c0 + c) / 8] = w4[c / 8];
-          }
-          // next row f4: the same row into every peer's output buffer (another
-          // rank's buffer mapped into this process: the stores go over NVLink)
-          for (int i = 0; i < n_peer; ++i) {
-            uint4* pd = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(__ldg(peer_o + i)) + off);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) pd[c0 / 8 + c] = w4[c];
-          }
-        }
-      }
-    }
   }
   tc_fence_before();
   __syncthreads();
@@ -680,26 +724,36 @@ extern "C" int fp_debug_attn8_timing(unsigned long long* out, int reset) {
 cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
-                           const void* const* peer_o, int n_peer, cudaStream_t st) {
+                           const void* const* peer_o, int n_peer, int* work_counter, cudaStream_t st) {
   const size_t smem = attn8_smem_bytes();
   cudaError_t ea = ensure_smem_attr((const void*)attn8_kernel<true>, smem);
   if (ea == cudaSuccess) ea = ensure_smem_attr((const void*)attn8_kernel<false>, smem);
   if (ea != cudaSuccess) return ea;
+  int dev = 0, nsm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
-  const dim3 grid(s.H * ((s.nb + 1) / 2));
+  const int total = s.H * ((s.nb + 1) / 2);
+  // persistent (one CTA per SM, dynamic work fetch) when a workspace holds the
+  // work counter; otherwise one CTA per item (a static round-robin over a
+  // persistent grid would leave the per-item cost variance unbalanced)
+  const dim3 grid(work_counter ? std::min(total, nsm) : total);
+  if (work_counter) {
+    const cudaError_t em = cudaMemsetAsync(work_counter, 0, sizeof(int), st);
+    if (em != cudaSuccess) return em;
+  }
   auto* op = reinterpret_cast<__nv_bfloat16*>(o);
   if (dense)
     attn8_kernel<true><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
                                                       lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
                                                       row_ptr, col_idx, scale_log2,
                                                       reinterpret_cast<const unsigned long long*>(peer_o),
-                                                      n_peer);
+                                                      n_peer, total, work_counter);
   else
     attn8_kernel<false><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
                                                        lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
                                                        row_ptr, col_idx, scale_log2,
                                                        reinterpret_cast<const unsigned long long*>(peer_o),
-                                                       n_peer);
+                                                       n_peer, total, work_counter);
   return cudaGetLastError();
 }
 

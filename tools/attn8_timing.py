@@ -20,12 +20,15 @@ ap.add_argument("lib")
 ap.add_argument("--workload", default="C3-llama8b-128k")
 ap.add_argument("--dense", action="store_true")
 ap.add_argument("--v11", action="store_true")
+ap.add_argument("--seq-len", type=int, default=None)
 a = ap.parse_args()
 fp.load_library(os.path.abspath(a.lib))
 import torch  # noqa: E402
 from synth import gen, configs  # noqa: E402
 
 w = configs.get(a.workload)
+if a.seq_len:
+    w = w.with_(seq_len=a.seq_len)
 q, k, v = (torch.from_numpy(x).view(torch.bfloat16).cuda() for x in gen.make_layer_bits(w))
 fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len)
 out = torch.empty_like(q)

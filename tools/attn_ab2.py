@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("libs", nargs="+")
 ap.add_argument("--workload", default="C3-llama8b-128k")
 ap.add_argument("--gamma", type=float, default=None)
+ap.add_argument("--seq-len", type=int, default=None)
 ap.add_argument("--reps", type=int, default=12)
 ap.add_argument("--dense", action="store_true")
 ap.add_argument("--block", type=int, default=128)
@@ -33,6 +34,8 @@ from synth import gen, configs  # noqa: E402
 w = configs.get(a.workload)
 if a.gamma is not None:
     w = w.with_(gamma=a.gamma)
+if a.seq_len is not None:
+    w = w.with_(seq_len=a.seq_len)
 q, k, v = (torch.from_numpy(x).view(torch.bfloat16).cuda() for x in gen.make_layer_bits(w))
 fpl = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len, block_size=a.block)
 out = torch.empty_like(q)
@@ -51,7 +54,7 @@ st = torch.cuda.current_stream().cuda_stream
 def call(L):
     if a.dense:
         r = L.fp_dense_causal_attn(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), w.heads,
-                                   w.kv_heads, w.seq_len, 128, 128, None, 0, st)
+                                   w.kv_heads, w.seq_len, 128, 128, fpl.ws.data_ptr(), fpl.ws_bytes, st)
     else:
         r = L.fp_sparse_attn(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), w.heads,
                              w.kv_heads, w.seq_len, 128, a.block, fpl.row_ptr.data_ptr(),
