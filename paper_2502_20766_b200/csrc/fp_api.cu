@@ -413,9 +413,13 @@ fp_status fp_layer_host(const void* q_host, const void* k_host, const void* v_ho
       st = fp_select(ch.nh, 1, seq_len, head_dim, block_size, gamma, min_budget, wsc, slot, rp, ci,
                      nullptr, scomp);
     chk(cudaStreamWaitEvent(scomp, e_v, 0));
+    // one attention launch per head (the chunk's workspace slot holds the
+    // persistent scheduler's work counter), each head's output copied back as
+    // soon as it is done: measured faster than one launch + one copy per chunk
+    // (39.7 vs 40.6 ms at C3), the exposed tail is one head's download
     for (int i = 0; i < ch.nh && e == cudaSuccess && st == FP_OK; ++i) {
       st = fp_sparse_attn(qd + i * hb, kd, vd, od + i * hb, 1, 1, seq_len, head_dim, block_size,
-                          rp + (size_t)i * (nb + 1), ci + (size_t)i * cap, nullptr, 0, scomp);
+                          rp + (size_t)i * (nb + 1), ci + (size_t)i * cap, wsc, slot, scomp);
       chk(cudaEventRecord(e_h, scomp));
       chk(cudaStreamWaitEvent(sout, e_h, 0));
       chk(cudaMemcpyAsync(static_cast<char*>(o_host) + c * qb_bytes + (ch.h0 + i) * hb, od + i * hb,
