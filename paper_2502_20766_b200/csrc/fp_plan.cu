@@ -4,12 +4,12 @@
 // Query-Aware pooled map of Alg. 4 for QA heads.
 //
 // Kernels (one stream, no host sync):
-//   rep_pass<1>   N1a  S = Q^ K^T per (key chunk, head) on tcgen05 -> partial
-//                      row max / sum-exp; first head of each KV group also
-//                      writes the avg-pooled keys K_bar
-//   rep_stats         combine partials -> per-row max and 1/sum (fixed order)
-//   rep_pass<2>   N1b  S^T = K Q^T per (key chunk, head) -> p = softmax entries,
-//                      a_v (column sums) and per-tile slash (diagonal) partials
+//   rep1_kernel   N1a  (fp_rep.cu) S = Q^ K^T per (key chunk, KV group, <= 4
+//                      heads) on tcgen05 -> partial row max / sum-exp
+//   rep_stats         combine partials -> per-row max and M' = max + log2(sum)
+//   rep2_kernel   N1b  (fp_rep.cu) S^T = K Q^T per (key chunk, KV group, <= 2
+//                      heads) -> p, a_v (column sums), per-tile slash
+//                      partials; the first subset of a group writes K_bar
 //   slash_combine     a_s[o] from the overlapping tile partials (fixed order)
 //   block_sums        a_hat[kb] = sum of a_v over kb (A2); As[D] (A12)
 //   pattern_kernel N3 a_bar = softmax(avgpool(Q^) K_bar^T / sqrt d), D_JS, decision
