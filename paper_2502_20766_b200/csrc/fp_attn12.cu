@@ -1,0 +1,732 @@
+// fp_attn12.cu -- stage (iii) of FlexPrefill, y = A(Q, K, V, S) (P:66-83,
+// P:287-288), version 12: v8 (fp_attn8.cu: persistent q-block pairs sharing
+// their K/V loads, ping-pong rows, P in two halves) with FOUR softmax
+// warpgroups -- two per row, each owning 64 of the 128 keys of every tile.
+//
+// Why: v8's row period is its softmax (~2,500 cycles per tile of work: TMEM
+// load, max, rescale check, 128 exponentials, P stores) plus the row's PV + S
+// on the tensor core (~1,000), in series (one S buffer per row). Splitting the
+// tile's keys over two warpgroups halves the exponentials and stores on the
+// row's critical path; the row max is exchanged through shared memory (one
+// named barrier per tile and row), each half keeps its own partial row sum
+// (added once in the epilogue), rescales and stores its own 64 columns of O.
+// P of keys 0-63 (warpgroup X0) releases the PV's first four k-steps (p_lo),
+// keys 64-127 (X1) the second four (p_full) -- v8's P halves.
+// 640 threads: warps 0-3 A0, 4-7 A1, 8-11 B0, 12-15 B1, 16 K producer,
+// 17 MMA issuer, 18 V producer.
+#include <math.h>
+
+#include <algorithm>
+
+#include "fp_common.cuh"
+#include "fp_internal.h"
+
+#ifdef FP_TIMING
+// clock64 phase accumulators (tools/attn8_timing.py): [0..5] softmax thread 0
+// of each row, [8..12] the MMA issuer, [14] issuer entries, [15] softmax tiles
+__device__ unsigned long long g_attn12_timing[16];
+#define FP_T8(k) do { if (t_on) { long long _t = clock64(); tacc[k] += _t - tlast; tlast = _t; } } while (0)
+#define FP_T8_DECL(on) const bool t_on = (on); long long tacc[16] = {0}; long long tlast = clock64()
+#define FP_T8_FLUSH(lo, hi) do { if (t_on) for (int _k = lo; _k < hi; ++_k) atomicAdd(&g_attn12_timing[_k], (unsigned long long)tacc[_k]); } while (0)
+#else
+#define FP_T8(k) do { } while (0)
+#define FP_T8_DECL(on) do { } while (0)
+#define FP_T8_FLUSH(lo, hi) do { } while (0)
+#endif
+
+namespace fp {
+
+namespace {
+
+constexpr int kThreads8 = 640;
+#ifndef FP_EMU12
+#define FP_EMU12 0
+#endif
+constexpr int kEmu12 = FP_EMU12;  // exponentials per 32-key chunk on the FMA pipe
+constexpr int kKS8 = 2, kVS8 = 3;  // K / V ring depths (tiles)
+constexpr uint32_t kColS8 = 0, kColO8 = 256;
+constexpr float kRescale8 = 8.0f;  // lazy rescale: tolerate P up to 2^8 (as v5)
+// exponentials per row and tile (of 128) computed on the FMA pipe instead of
+// the MUFU (16 ex2/clk/SM, the softmax floor: 1024 cycles per 128x128 tile).
+// Measured on B200 (tools/attn_ab2.py block timing, C3 gamma 0.95): 0 -> 34.3
+// ms, 16 -> 34.5, 32 -> 35.5 (dense: 115.4 -> 120.9 at 32): under the 1 kW
+// power cap the extra FMA-pipe work lowers the clock more than it saves.
+#ifndef FP_EMU8
+#define FP_EMU8 0
+#endif
+constexpr int kEmu8 = FP_EMU8;
+// P handed to the tensor core in two halves (keys 0-63, 64-127): the softmax
+// stores P in 32-key chunks as the exponentials finish (tcgen05.st overlaps
+// the next chunk's MUFU work) and arrives on p_lo once the first half is
+// stored (checked after chunk 2's exponentials, so the wait does not stall), so
+// the issuer starts PV's first four k-steps while the second half is still
+// being exponentiated. Bitwise equal to the unsplit path; measured (C3,
+// alternating 12-launch blocks) 34.04-34.19 ms vs 34.20-34.79 ms sparse, equal
+// dense (profiles/r01_v8_phase_timing.txt). The gain is small because a row's
+// period is bound by its single S buffer (S(e+1) waits for softmax(e) and
+// PV(e)): the MMA pipeline alone runs at 3147 cycles per union entry against
+// 2048 of tensor work (the -DFP_XSM8 experiment), see DESIGN.md section 6.
+#ifndef FP_SPLIT8
+#define FP_SPLIT8 1
+#endif
+constexpr bool kSplit8 = FP_SPLIT8 != 0;
+
+struct Attn12Smem {
+  uint8_t q[2][kTileBytes];  // Q_A, Q_B (1024-B aligned: first member)
+  uint8_t k[kKS8][kTileBytes];
+  uint8_t v[kVS8][kTileBytes];
+  uint64_t q_full, q_empty;
+  uint64_t item_full[2], item_empty[2];  // work-item id ring (persistent scheduling)
+  int item[2];
+  // [row][half][query row]: row-max exchange per tile, row-sum exchange in the
+  // epilogue. One buffer suffices: a half can only reach tile t + 1 after the
+  // other half released P(t) (S(t + 1) follows PV(t)), i.e. after it read
+  // the max of tile t.
+  float xch[2][2][128];
+  uint64_t k_full[kKS8], k_empty[kKS8];
+  uint64_t v_full[kVS8], v_empty[kVS8];
+  uint64_t s_full[2], p_full[2], p_lo[2], pv_done[2];
+  uint32_t tmem_base;
+};
+
+FP_DEV float fmax3_8(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+FP_DEV void ffma2_8(float& d0, float& d1, float a0, float a1, float b, float c) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %4};\n\tmov.b64 rc, {%5, %5};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b), "f"(c));
+}
+FP_DEV void fadd2_8(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+FP_DEV void ffma2v_8(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+// 2^x for a pair on the FMA/ALU pipes (FlashAttention-4's MUFU offload):
+// x = j + f (j = rint(x), |f| <= 1/2), 2^f by a degree-3 minimax polynomial
+// (max rel. error 7.5e-5; P is rounded to bf16 afterwards, 2^-9), 2^j added
+// into the exponent field. x is clamped at -125 (masked keys are zeroed
+// separately on the diagonal block).
+FP_DEV void exp2_emu2_8(float x0, float x1, float& y0, float& y1) {
+  const float kMagic = 12582912.0f;  // 1.5 * 2^23: rounds to an integer in the low mantissa bits
+  x0 = fmaxf(x0, -125.0f);
+  x1 = fmaxf(x1, -125.0f);
+  float t0, t1, j0, j1, f0, f1, p0, p1;
+  fadd2_8(t0, t1, x0, x1, kMagic, kMagic);
+  fadd2_8(j0, j1, t0, t1, -kMagic, -kMagic);
+  fadd2_8(f0, f1, x0, x1, -j0, -j1);
+  ffma2_8(p0, p1, f0, f1, 0.0551716626f, 0.242611155f);
+  ffma2v_8(p0, p1, p0, p1, f0, f1, 0.69326099f, 0.69326099f);
+  ffma2v_8(p0, p1, p0, p1, f0, f1, 0.999928072f, 0.999928072f);
+  y0 = __uint_as_float(__float_as_uint(t0) * 8388608u + __float_as_uint(p0));
+  y1 = __uint_as_float(__float_as_uint(t1) * 8388608u + __float_as_uint(p1));
+}
+FP_DEV void tmem_ld_32x32b_x64_8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 " FP_REGLIST64 ", [%64];"
+               : FP_R64(r)
+               : "r"(taddr));
+}
+FP_DEV void tmem_st_32x32b_x64_8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x64.b32 [%64], " FP_REGLIST64 ";"
+               :
+               : FP_W64(r), "r"(taddr));
+}
+
+// S = Q K^T, M=128 N=128, 8 k-steps of 16 in one asm statement, both operands
+// K-major SW128 tiles of two 16 KiB boxes in smem: k-step kk at box kk/4, byte
+// (kk%4)*32 (descriptor start-address offsets in 16-B units: 2, 4, 6, 1024...).
+FP_DEV void umma_ss_chain8(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %9, %17, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %10, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %11, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %12, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %13, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %14, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %15, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %16, %17, p;\n\t}" ::"r"(d),
+      "l"(a0), "l"(a0 + 2), "l"(a0 + 4), "l"(a0 + 6), "l"(a0 + 1024), "l"(a0 + 1026),
+      "l"(a0 + 1028), "l"(a0 + 1030), "l"(b0), "l"(b0 + 2), "l"(b0 + 4), "l"(b0 + 6),
+      "l"(b0 + 1024), "l"(b0 + 1026), "l"(b0 + 1028), "l"(b0 + 1030), "r"(idesc));
+}
+// O += P V, M=128 N=128, 8 k-steps (16 keys each): A = P in TMEM columns
+// a0 + 8 kk, B = V (MN-major SW128) descriptor b0 + kk * 2048 B.
+FP_DEV void umma_pv_chain8(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %18, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %9, %17, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %10, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %11, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %12, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %13, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %14, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %15, %17, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %16, %17, p;\n\t}" ::"r"(d),
+      "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "r"(a0 + 32), "r"(a0 + 40), "r"(a0 + 48),
+      "r"(a0 + 56), "l"(b0), "l"(b0 + 128), "l"(b0 + 256), "l"(b0 + 384), "l"(b0 + 512),
+      "l"(b0 + 640), "l"(b0 + 768), "l"(b0 + 896), "r"(idesc), "r"(acc0));
+}
+
+// The MMA issuer runs as a whole warp (FP_WARPISSUE8, default): every lane
+// executes the same loop on the same (warp-uniform) values and the MMA /
+// commit instructions are predicated on elect.sync inside the asm. With the
+// issuer under `if (lane_id() == 0)` instead, the descriptors live in
+// per-thread registers and ptxas wraps every tcgen05.mma in an R2UR +
+// elect/branch loop: ~52 cycles to issue one MMA (tools/attn8_timing.py),
+// which made the single issuing thread the bottleneck of the kernel.
+#ifndef FP_WARPISSUE8
+#define FP_WARPISSUE8 1
+#endif
+constexpr bool kWarpIssue8 = FP_WARPISSUE8 != 0;
+#define FP_ELECT "elect.sync _|ep, 0xffffffff;\n\t"
+FP_DEV void umma_ss_chain8_w(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, 1, 0;\n\t" FP_ELECT
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %9, %17, 0;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %10, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %11, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %12, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %13, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %14, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %15, %17, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %16, %17, p;\n\t}" ::"r"(d),
+      "l"(a0), "l"(a0 + 2), "l"(a0 + 4), "l"(a0 + 6), "l"(a0 + 1024), "l"(a0 + 1026),
+      "l"(a0 + 1028), "l"(a0 + 1030), "l"(b0), "l"(b0 + 2), "l"(b0 + 4), "l"(b0 + 6),
+      "l"(b0 + 1024), "l"(b0 + 1026), "l"(b0 + 1028), "l"(b0 + 1030), "r"(idesc));
+}
+FP_DEV void umma_pv_chain4_w(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q, ep;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t" FP_ELECT
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %9, q;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %6, %9, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %7, %9, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %8, %9, p;\n\t}" ::"r"(d),
+      "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "l"(b0), "l"(b0 + 128), "l"(b0 + 256),
+      "l"(b0 + 384), "r"(idesc), "r"(acc0));
+}
+FP_DEV void umma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred ep;\n\t" FP_ELECT
+      "@ep tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+// Half of O += P V: 4 k-steps (64 keys) starting at P column a0 / V descriptor b0.
+FP_DEV void umma_pv_chain4(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %9, q;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %6, %9, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %7, %9, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %8, %9, p;\n\t}" ::"r"(d),
+      "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "l"(b0), "l"(b0 + 128), "l"(b0 + 256),
+      "l"(b0 + 384), "r"(idesc), "r"(acc0));
+}
+
+#define PVCHAIN4(...) (kWarpIssue8 ? umma_pv_chain4_w(__VA_ARGS__) : umma_pv_chain4(__VA_ARGS__))
+#define SSCHAIN8(...) (kWarpIssue8 ? umma_ss_chain8_w(__VA_ARGS__) : umma_ss_chain8(__VA_ARGS__))
+#define COMMIT8(b) (kWarpIssue8 ? umma_commit_w(b) : umma_commit(b))
+
+// Merge of the two rows' sorted key-block lists: next union entry.
+// mask bit 0: row A selected it, bit 1: row B. The list heads are loaded one
+// entry ahead, so the global-load latency overlaps the caller's work.
+struct UnionIter {
+  const int32_t* la;
+  const int32_t* lb;
+  int na, nb_, ia, ib;
+  bool dense;
+  int ca, cb;  // key blocks at ia / ib (INT_MAX past the end)
+  FP_DEV void init(const int32_t* a_, const int32_t* b_, int na_, int nb2, bool d) {
+    la = a_;
+    lb = b_;
+    na = na_;
+    nb_ = nb2;
+    ia = ib = 0;
+    dense = d;
+    ca = na > 0 ? (dense ? 0 : __ldg(la)) : 0x7fffffff;
+    cb = nb_ > 0 ? (dense ? 0 : __ldg(lb)) : 0x7fffffff;
+  }
+  FP_DEV bool done() const { return ia >= na && ib >= nb_; }
+  FP_DEV int next(int& mask) {
+    const int k = min(ca, cb);
+    mask = (ca == k ? 1 : 0) | (cb == k ? 2 : 0);
+    if (mask & 1) {
+      ++ia;
+      ca = ia < na ? (dense ? ia : __ldg(la + ia)) : 0x7fffffff;
+    }
+    if (mask & 2) {
+      ++ib;
+      cb = ib < nb_ ? (dense ? ib : __ldg(lb + ib)) : 0x7fffffff;
+    }
+    return k;
+  }
+};
+
+// One work item = (head h, q-block pair (qbA, qbB = qbA - 1)); items are
+// numbered KV-group-major, pairs descending, heads of a group interleaved (the
+// K/V of one group, 64 MiB at 128k, stay in L2 while its items run).
+struct Item {
+  int h, g, qbA, qbB, nA, nB;
+  const int32_t* la;
+  const int32_t* lb;
+};
+template <bool DENSE>
+FP_DEV Item decode_item(int item, int H, int G, int nb, long long cap, const int32_t* row_ptr,
+                        const int32_t* col_idx) {
+  Item it;
+  const int gsz = H / G;
+  const int npair = (nb + 1) >> 1;
+  const int per_group = gsz * npair;
+  it.g = item / per_group;
+  const int rem = item - it.g * per_group;
+  it.qbA = nb - 1 - 2 * (rem / gsz);
+  it.qbB = it.qbA - 1;  // -1: no row B
+  it.h = it.g * gsz + rem % gsz;
+  it.la = it.lb = nullptr;
+  if (DENSE) {
+    it.nA = it.qbA + 1;
+    it.nB = it.qbB + 1;
+  } else {
+    const int32_t* rp = row_ptr + (size_t)it.h * (nb + 1);
+    const int bA = __ldg(rp + it.qbA);
+    it.nA = __ldg(rp + it.qbA + 1) - bA;
+    it.la = col_idx + (size_t)it.h * cap + bA;
+    if (it.qbB >= 0) {
+      const int bB = __ldg(rp + it.qbB);
+      it.nB = bA - bB;
+      it.lb = col_idx + (size_t)it.h * cap + bB;
+    } else {
+      it.nB = 0;
+    }
+  }
+  return it;
+}
+
+// Persistent: gridDim.x <= #SMs CTAs (one per SM), each runs work items until
+// the list is exhausted. Items come from an atomic counter in the workspace
+// (work_counter, zeroed before the launch: dynamic balancing, the next item
+// goes to the first free SM). Without a workspace the grid has one CTA per
+// item (item = blockIdx.x). Warp 8 fetches the ids and publishes them through a 2-slot
+// ring (item_full / item_empty); every barrier phase below is counted
+// cumulatively over the CTA's items. Across items: the next item's Q tiles
+// are loaded once the last S MMA of the current one completed (q_empty), its
+// first S MMAs run while the softmax warpgroups finish the current item, and
+// a row's O is overwritten (first PV, accumulate = 0) only after its P -- which
+// the warpgroup produces after its previous epilogue read O -- is stored.
+template <bool DENSE>
+__global__ void __launch_bounds__(kThreads8, 1)
+    attn12_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                 const __grid_constant__ CUtensorMap vmap, __nv_bfloat16* __restrict__ o,
+                 const TLayout ol, int Hp, int Gp, int H, int G, int n, int nb, long long cap,
+                 const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                 float scale_log2, const unsigned long long* __restrict__ peer_o, int n_peer,
+                 int total_items, int* __restrict__ work_counter) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 tiles need 1024-B alignment
+  Attn12Smem& sm = *reinterpret_cast<Attn12Smem*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int wid = warp_id();
+
+  if (wid == 17) tmem_alloc(&sm.tmem_base, 512);
+  if (tid == 512) {
+    tma_prefetch_desc(&qmap);
+    tma_prefetch_desc(&kmap);
+    tma_prefetch_desc(&vmap);
+    mbar_init(&sm.q_full, 1);
+    mbar_init(&sm.q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.item_full[i], 1);
+      mbar_init(&sm.item_empty[i], 18);  // V producer, issuer, 16 softmax warps
+    }
+    for (int s = 0; s < kKS8; ++s) {
+      mbar_init(&sm.k_full[s], 1);
+      mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < kVS8; ++s) {
+      mbar_init(&sm.v_full[s], 1);
+      mbar_init(&sm.v_empty[s], 2);  // two commits per entry (see the issuer)
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&sm.s_full[x], 1);
+      mbar_init(&sm.p_full[x], 4);  // P of keys 64-127: the 4 warps of warpgroup X1
+      mbar_init(&sm.p_lo[x], 4);    // P of keys 0-63: the 4 warps of warpgroup X0
+      mbar_init(&sm.pv_done[x], 1);
+    }
+    mbar_fence_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = sm.tmem_base;
+  // consumers: the k-th item id of this CTA (-1: no more work)
+  auto get_item = [&](int k) {
+    mbar_wait(&sm.item_full[k & 1], (k >> 1) & 1);
+    return sm.item[k & 1];
+  };
+
+  if (wid >= 16) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (wid == 16 || wid == 18) {
+      // ------------------------------------------------ TMA producers (K: warp 8, V: warp 10)
+      if (lane_id() == 0) {
+        const bool isK = (wid == 16);
+        const uint64_t pol = policy_evict_last();
+        const int depth = isK ? kKS8 : kVS8;
+        uint64_t* full = isK ? sm.k_full : sm.v_full;
+        uint64_t* empty = isK ? sm.k_empty : sm.v_empty;
+        const CUtensorMap* map = isK ? &kmap : &vmap;
+        int e = 0;  // union entries loaded so far (all items)
+        for (int k = 0;; ++k) {
+          int item;
+          if (isK) {
+            // scheduler: fetch the k-th item and publish it
+            item = work_counter ? atomicAdd(work_counter, 1) : (int)blockIdx.x + k * (int)gridDim.x;
+            if (item >= total_items) item = -1;
+            if (k >= 2) mbar_wait(&sm.item_empty[k & 1], ((k - 2) >> 1) & 1);
+            sm.item[k & 1] = item;
+            mbar_arrive(&sm.item_full[k & 1]);
+          } else {
+            item = get_item(k);
+            mbar_arrive(&sm.item_empty[k & 1]);
+          }
+          if (item < 0) break;
+          const Item it = decode_item<DENSE>(item, H, G, nb, cap, row_ptr, col_idx);
+          if (isK) {
+            // Q_A, Q_B of this item once the previous item's S MMAs are done
+            if (k >= 1) mbar_wait(&sm.q_empty, (k - 1) & 1);
+            mbar_arrive_expect_tx(&sm.q_full, it.nB > 0 ? 2 * kTileBytes : kTileBytes);
+            tma_tile(sm.q[0], &qmap, &sm.q_full, it.qbA * 128, it.h, Hp);
+            if (it.nB > 0) tma_tile(sm.q[1], &qmap, &sm.q_full, it.qbB * 128, it.h, Hp);
+          }
+          UnionIter un;
+          un.init(it.la, it.lb, it.nA, it.nB, DENSE);
+          for (; !un.done(); ++e) {
+            int mask;
+            const int kb = un.next(mask);
+            const int s = e % depth;
+            if (e >= depth) mbar_wait(&empty[s], ((e - depth) / depth) & 1);
+            mbar_arrive_expect_tx(&full[s], kTileBytes);
+            tma_tile_hint(isK ? sm.k[s] : sm.v[s], map, &full[s], kb * 128, it.g, Gp, pol);
+          }
+        }
+        // drain: the issuer releases every slot it consumes (it does not know
+        // the union length); consume those releases before the CTA exits
+        for (int d = max(0, e - depth); d < e; ++d) mbar_wait(&empty[d % depth], (d / depth) & 1);
+      }
+    } else if (wid == 17) {
+      // ------------------------------------------------ MMA issuer
+      if (kWarpIssue8 || lane_id() == 0) {
+        constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false);
+        constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, true);
+        const uint64_t qdesc[2] = {sdesc_kmajor(smem_u32(sm.q[0]), 0), sdesc_kmajor(smem_u32(sm.q[1]), 0)};
+        int cnt[2] = {0, 0};     // S tiles issued per stream (all items)
+        int e = 0;               // union entries consumed (all items)
+        FP_T8_DECL(lane_id() == 0);
+        for (int k = 0;; ++k) {
+          const int item = get_item(k);
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
+          if (item < 0) break;
+          const Item itm = decode_item<DENSE>(item, H, G, nb, cap, row_ptr, col_idx);
+          int pend[2] = {-1, -1};  // union entry of X's S awaiting its PV
+          int lcnt[2] = {0, 0};    // S tiles issued per stream in this item
+          auto issue_pv = [&](int x) {
+            const int ep = pend[x];
+            const int vs = ep % kVS8;
+            FP_T8(12);
+            mbar_wait(&sm.v_full[vs], (ep / kVS8) & 1);
+            FP_T8(9);
+            const uint64_t vdesc = sdesc_mnmajor(smem_u32(sm.v[vs]), 0);
+            if (kSplit8) {
+              mbar_wait(&sm.p_lo[x], (cnt[x] - 1) & 1);
+              FP_T8(10);
+              tc_fence_after();
+              PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o, lcnt[x] > 1);
+              FP_T8(12);
+              mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
+              FP_T8(11);
+              tc_fence_after();
+              PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512, idesc_o, 1);
+            } else {
+              mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
+              tc_fence_after();
+              umma_pv_chain8(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
+                             lcnt[x] > 1);
+            }
+            COMMIT8(&sm.v_empty[vs]);
+            COMMIT8(&sm.pv_done[x]);
+            pend[x] = -1;
+          };
+          mbar_wait(&sm.q_full, k & 1);
+          UnionIter un;
+          un.init(itm.la, itm.lb, itm.nA, itm.nB, DENSE);
+          for (; !un.done(); ++e) {
+            int mask;
+            un.next(mask);
+            const int ks = e % kKS8;
+            FP_T8(12);
+            mbar_wait(&sm.k_full[ks], (e / kKS8) & 1);
+            FP_T8(8);
+#ifdef FP_TIMING
+            ++tacc[14];
+#endif
+            tc_fence_after();
+            const uint64_t kdesc = sdesc_kmajor(smem_u32(sm.k[ks]), 0);
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+              if (pend[x] >= 0) issue_pv(x);
+              if (mask & (1 << x)) {
+                FP_T8(12);
+#if !defined(FP_XMMA8) && !defined(FP_XS8)
+                SSCHAIN8(tbase + kColS8 + x * 128, qdesc[x], kdesc, idesc_s);
+#endif
+                FP_T8(13);  // issue time of the 8 S MMAs
+                COMMIT8(&sm.s_full[x]);
+                pend[x] = e;
+                ++cnt[x];
+                ++lcnt[x];
+              }
+            }
+            COMMIT8(&sm.k_empty[ks]);
+            // an entry only one row uses gets its second V-slot release here
+            // (it arrives early, but the phase also needs the PV's commit)
+            if (mask != 3) COMMIT8(&sm.v_empty[e % kVS8]);
+          }
+          // every S MMA of this item is issued: Q may be reloaded once they complete
+          COMMIT8(&sm.q_empty);
+          if (pend[0] >= 0) issue_pv(0);
+          if (pend[1] >= 0) issue_pv(1);
+        }
+        FP_T8(12);
+        FP_T8_FLUSH(8, 15);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+    // ------------------------------------------------ softmax warpgroups
+    const int x = wid >> 3;                     // 0 = row A, 1 = row B
+    const int hf = (wid >> 2) & 1;              // key half of every tile: 64 hf .. 64 hf + 63
+    const int r = (wid & 3) * 32 + lane_id();   // query row within the block = TMEM lane
+    const uint32_t lane_off = (uint32_t)((wid & 3) * 32) << 16;
+    const uint32_t tS = tbase + kColS8 + x * 128 + lane_off;
+    const uint32_t tO = tbase + kColO8 + x * 128 + lane_off + hf * 64;
+    int T = 0;  // tiles of this row processed in earlier items (barrier phases)
+    FP_T8_DECL((wid & 7) == 0 && lane_id() == 0);
+    for (int k = 0;; ++k) {
+      const int item = get_item(k);
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
+      if (item < 0) break;
+      const Item itm = decode_item<DENSE>(item, H, G, nb, cap, row_ptr, col_idx);
+      const int nX = x ? itm.nB : itm.nA;
+      const int qb = x ? itm.qbB : itm.qbA;
+      float m_used = -INFINITY, l = 0.f;
+      for (int t = 0; t < nX; ++t) {
+        const int ph = (T + t) & 1;  // this tile's phase of s_full / p_lo / p_full
+        FP_T8(6);
+        mbar_wait(&sm.s_full[x], ph);
+        FP_T8(0);
+        tc_fence_after();
+        float v[64];
+        tmem_ld_32x32b_x64_8(tS + hf * 64, reinterpret_cast<uint32_t*>(v));
+        // probe pv_done(t - 1) now (complete: S(t) followed PV(t - 1) in the
+        // in-order MMA stream) so the probe's latency overlaps the TMEM load
+        const bool pv_ok = t == 0 || mbar_try_wait(smem_u32(&sm.pv_done[x]), (T + t - 1) & 1);
+        tmem_wait_ld();
+        FP_T8(1);
+        if (t == nX - 1) {  // the diagonal block: keys j <= r only
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (hf * 64 + c > r) v[c] = -INFINITY;
+        }
+        // row max of this half: 8 independent fmax3 chains, then a tree; the
+        // other half's max through shared memory (one barrier per row and tile)
+        float mc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(v[8 * j], v[8 * j + 1], v[8 * j + 2]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(mc[j], v[8 * j + 3], v[8 * j + 4]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(mc[j], v[8 * j + 5], v[8 * j + 6]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mc[j] = fmaxf(mc[j], v[8 * j + 7]);
+        const float mh = fmaxf(fmax3_8(mc[0], mc[1], mc[2]), fmax3_8(mc[3], mc[4], fmax3_8(mc[5], mc[6], mc[7])));
+        sm.xch[x][hf][r] = mh;
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + x) : "memory");
+        const float mx = fmaxf(mh, sm.xch[x][hf ^ 1][r]) * scale_log2;
+        float alpha = 1.f;
+        if (mx > m_used + kRescale8) {
+          alpha = exp2f(m_used - mx);  // 0 on the first tile
+          m_used = mx;
+        }
+        const float nm = -m_used;
+        FP_T8(2);
+        // O_X holds sum_{earlier} P V: PV of the previous tile completed before
+        // S of this one; every pv_done phase is consumed
+        if (!pv_ok) mbar_wait(&sm.pv_done[x], (T + t - 1) & 1);
+        if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          tc_fence_after();
+#pragma unroll
+          for (int q2 = 0; q2 < 2; ++q2) {
+            uint32_t ov[32];
+            tmem_ld32(tO + q2 * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
+            tmem_st32(tO + q2 * 32, ov);
+          }
+        }
+        FP_T8(3);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const int c0 = ch * 32;
+#pragma unroll
+          for (int c = c0; c < c0 + 32; c += 2) ffma2_8(v[c], v[c + 1], v[c], v[c + 1], scale_log2, nm);
+#pragma unroll
+          for (int c = c0; c < c0 + 32 - kEmu12; ++c) v[c] = fast_exp2(v[c]);
+#pragma unroll
+          for (int c = c0 + 32 - kEmu12; c < c0 + 32; c += 2) exp2_emu2_8(v[c], v[c + 1], v[c], v[c + 1]);
+          if (kEmu12 > 0 && t == nX - 1) {  // masked keys of the diagonal block: exactly 0
+#pragma unroll
+            for (int c = c0 + 32 - kEmu12; c < c0 + 32; ++c)
+              if (hf * 64 + c > r) v[c] = 0.f;
+          }
+#pragma unroll
+          for (int c = c0; c < c0 + 32; c += 4) {
+            fadd2_8(s0, s1, s0, s1, v[c], v[c + 1]);
+            fadd2_8(s2, s3, s2, s3, v[c + 2], v[c + 3]);
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk[c] = pack_bf16x2(v[c0 + 2 * c], v[c0 + 2 * c + 1]);
+          tmem_st16(tS + hf * 32 + ch * 16, pk);  // P over S: keys 64 hf + 32 ch .. as 16 columns
+        }
+        l = l * alpha + ((s0 + s1) + (s2 + s3));
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(hf ? &sm.p_full[x] : &sm.p_lo[x]);
+        FP_T8(5);
+#ifdef FP_TIMING
+        ++tacc[15];
+#endif
+      }
+      if (nX > 0) {
+        // epilogue: the row sum of both halves, O / l of this half's 64
+        // columns -> bf16 -> global (rows past n are not stored)
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + x) : "memory");  // both halves read the last max
+        sm.xch[x][hf][r] = l;
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + x) : "memory");
+        const float il = 1.0f / (l + sm.xch[x][hf ^ 1][r]);
+        mbar_wait(&sm.pv_done[x], (T + nX - 1) & 1);
+        tc_fence_after();
+        const int row = qb * 128 + r;
+        const size_t off = toff(ol, itm.h, row) + hf * 64;
+        uint4* dst = reinterpret_cast<uint4*>(o + off);
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t ov[32];
+          tmem_ld32(tO + c0, ov);
+          tmem_wait_ld();
+          if (row < n) {
+            uint4 w4[4];
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                w[e] = pack_bf16x2(__uint_as_float(ov[c + 2 * e]) * il, __uint_as_float(ov[c + 2 * e + 1]) * il);
+              w4[c / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+              dst[(c0 + c) / 8] = w4[c / 8];
+            }
+            // next row f4: the same row into every peer's output buffer (another
+            // rank's buffer mapped into this process: the stores go over NVLink)
+            for (int i = 0; i < n_peer; ++i) {
+              uint4* pd = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(__ldg(peer_o + i)) + off);
+#pragma unroll
+              for (int c = 0; c < 4; ++c) pd[c0 / 8 + c] = w4[c];
+            }
+          }
+        }
+        tc_fence_before();  // O reads complete before P of the next item is released
+      }
+      T += nX;
+    }
+    FP_T8_FLUSH(0, 8);
+#ifdef FP_TIMING
+    if (t_on) atomicAdd(&g_attn12_timing[15], (unsigned long long)tacc[15]);
+#endif
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (wid == 17) tmem_dealloc(tbase, 512);
+}
+
+}  // namespace
+
+size_t attn12_smem_bytes() { return sizeof(Attn12Smem); }
+
+#ifdef FP_TIMING
+extern "C" int fp_debug_attn12_timing(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_attn12_timing, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_attn12_timing, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
+cudaError_t launch_attn_v12(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
+                           const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
+                           const int32_t* row_ptr, const int32_t* col_idx, bool dense,
+                           const void* const* peer_o, int n_peer, int* work_counter, cudaStream_t st) {
+  const size_t smem = attn12_smem_bytes();
+  cudaError_t ea = ensure_smem_attr((const void*)attn12_kernel<true>, smem);
+  if (ea == cudaSuccess) ea = ensure_smem_attr((const void*)attn12_kernel<false>, smem);
+  if (ea != cudaSuccess) return ea;
+  int dev = 0, nsm = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
+  const int total = s.H * ((s.nb + 1) / 2);
+  // persistent (one CTA per SM, dynamic work fetch) when a workspace holds the
+  // work counter; otherwise one CTA per item (a static round-robin over a
+  // persistent grid would leave the per-item cost variance unbalanced)
+  const dim3 grid(work_counter ? std::min(total, nsm) : total);
+  if (work_counter) {
+    const cudaError_t em = cudaMemsetAsync(work_counter, 0, sizeof(int), st);
+    if (em != cudaSuccess) return em;
+  }
+  auto* op = reinterpret_cast<__nv_bfloat16*>(o);
+  if (dense)
+    attn12_kernel<true><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
+                                                      lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
+                                                      row_ptr, col_idx, scale_log2,
+                                                      reinterpret_cast<const unsigned long long*>(peer_o),
+                                                      n_peer, total, work_counter);
+  else
+    attn12_kernel<false><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
+                                                       lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
+                                                       row_ptr, col_idx, scale_log2,
+                                                       reinterpret_cast<const unsigned long long*>(peer_o),
+                                                       n_peer, total, work_counter);
+  return cudaGetLastError();
+}
+
+}  // namespace fp
