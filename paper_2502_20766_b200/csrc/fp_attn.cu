@@ -11,10 +11,6 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
                            const void* const* peer_o, int n_peer, int* work_counter, cudaStream_t st);
-cudaError_t launch_attn_v12(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
-                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
-                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
-                            const void* const* peer_o, int n_peer, int* work_counter, cudaStream_t st);
 cudaError_t launch_attn_b64(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                             const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                             const int32_t* row_ptr, const int32_t* col_idx, cudaStream_t st);
@@ -32,11 +28,7 @@ cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layou
   const Shape s128 = s.b == 128 ? s : make_shape(s.H, s.G, s.n, 128);
   // work counter of the persistent scheduler (ws is optional scratch)
   int* counter = ws ? wsp<int>(ws, L.sched) : nullptr;
-#ifdef FP_ATTN_V12
-  return launch_attn_v12(s128, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, peer_o, n_peer, counter, st);
-#else
   return launch_attn_v8(s128, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, peer_o, n_peer, counter, st);
-#endif
 }
 
 }  // namespace fp

@@ -37,7 +37,7 @@ fpl.select(w.gamma, w.min_budget)
 run = (lambda: fpl.dense(q, k, v, out)) if a.dense else (lambda: fpl.attn(q, k, v, out))
 raw = ctypes.CDLL(os.path.abspath(a.lib))
 buf = (ctypes.c_ulonglong * 16)()
-dbg = getattr(raw, "fp_debug_attn12_timing", None) or raw.fp_debug_attn8_timing
+dbg = raw.fp_debug_attn8_timing
 run()
 torch.cuda.synchronize()
 dbg(buf, 1)
