@@ -15,7 +15,10 @@ from synth import configs, gen  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C2-llama8b-32k"
 heads = int(sys.argv[sys.argv.index("--heads") + 1]) if "--heads" in sys.argv else None
+seq = int(sys.argv[sys.argv.index("--seq-len") + 1]) if "--seq-len" in sys.argv else None
 w = configs.get(name)
+if seq:
+    w = w.with_(seq_len=seq)
 if heads:
     w = w.with_(heads=heads, kv_heads=max(1, heads * w.kv_heads // w.heads))
 fp.load_library()
