@@ -386,10 +386,17 @@ __global__ void __launch_bounds__(kThreads8, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = sm.tmem_base;
-  // consumers: the k-th item id of this CTA (-1: no more work)
+  // consumers: the k-th item id of this CTA (-1: no more work). Lane 0 reads
+  // the slot and broadcasts it, so the slot's only reader is the thread whose
+  // item_empty arrival (release) orders the read before the producer's next
+  // write of the slot.
   auto get_item = [&](int k) {
-    mbar_wait(&sm.item_full[k & 1], (k >> 1) & 1);
-    return sm.item[k & 1];
+    int v = 0;
+    if (lane_id() == 0) {
+      mbar_wait(&sm.item_full[k & 1], (k >> 1) & 1);
+      v = sm.item[k & 1];
+    }
+    return __shfl_sync(0xffffffffu, v, 0);
   };
 
   if (wid >= 8) {
@@ -414,7 +421,8 @@ __global__ void __launch_bounds__(kThreads8, 1)
             sm.item[k & 1] = item;
             mbar_arrive(&sm.item_full[k & 1]);
           } else {
-            item = get_item(k);
+            mbar_wait(&sm.item_full[k & 1], (k >> 1) & 1);  // V producer: lane 0 only
+            item = sm.item[k & 1];
             mbar_arrive(&sm.item_empty[k & 1]);
           }
           if (item < 0) break;

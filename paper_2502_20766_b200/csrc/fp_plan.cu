@@ -267,29 +267,29 @@ __global__ void __launch_bounds__(64) pooled_logits(
   while ((rt + 1) * (rt + 2) / 2 <= (int)blockIdx.x) ++rt;
   while (rt * (rt + 1) / 2 > (int)blockIdx.x) --rt;
   const int ct = (int)blockIdx.x - rt * (rt + 1) / 2;
-  __shared__ __align__(16) float qs[kPT][132];
-  __shared__ __align__(16) float ks[kPT][132];
+  // transposed float4 tiles [d / 4][row]: the 4 x 4 register tiles read 4 / 8
+  // consecutive float4s per warp instruction (conflict-free shared loads)
+  __shared__ float4 qs4[32][kPT];
+  __shared__ float4 ks4[32][kPT];
   const int g = h / (H / G);
   const int tid = threadIdx.x;
   for (int e = tid; e < kPT * 32; e += 64) {
     const int rr = e >> 5, d4 = e & 31;
     const int qb = rt * kPT + rr, kb = ct * kPT + rr;
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(&qs[rr][d4 * 4]) =
-        qb < nb ? __ldg(reinterpret_cast<const float4*>(q_bar + ((size_t)h * nb + qb) * 128) + d4) : zero;
-    *reinterpret_cast<float4*>(&ks[rr][d4 * 4]) =
-        kb < nb ? __ldg(reinterpret_cast<const float4*>(k_bar + ((size_t)g * nb + kb) * 128) + d4) : zero;
+    qs4[d4][rr] = qb < nb ? __ldg(reinterpret_cast<const float4*>(q_bar + ((size_t)h * nb + qb) * 128) + d4) : zero;
+    ks4[d4][rr] = kb < nb ? __ldg(reinterpret_cast<const float4*>(k_bar + ((size_t)g * nb + kb) * 128) + d4) : zero;
   }
   __syncthreads();
   const int r0 = (tid >> 3) * 4, c0 = (tid & 7) * 4;
   float acc[4][4] = {};
 #pragma unroll 4
-  for (int d = 0; d < 128; d += 4) {
+  for (int d4 = 0; d4 < 32; ++d4) {
     float4 qv[4], kv[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      qv[i] = *reinterpret_cast<const float4*>(&qs[r0 + i][d]);
-      kv[i] = *reinterpret_cast<const float4*>(&ks[c0 + i][d]);
+      qv[i] = qs4[d4][r0 + i];
+      kv[i] = ks4[d4][c0 + i];
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
