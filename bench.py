@@ -239,7 +239,8 @@ def config_dict(w, world, dist_on, balance="static"):
         par = "single GPU"
     elif balance == "static":
         par = (f"Q heads partitioned over {world} ranks with their GQA KV groups (contiguous, "
-               "balanced) + one NCCL all_gather_into_tensor of O")
+               "balanced) + NCCL all_gather_into_tensor of O in <= 4 head chunks, each overlapped "
+               "with the next chunk's attention")
     else:
         par = f"LPT heads over {world} ranks (f4)"
     return dict(w.describe(), parallelism=par, l2=l2_note(w))
@@ -577,6 +578,52 @@ def main():
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    # N > 1: the output all-gather overlaps the attention. The rank's head slots
+    # [0, hmax) are cut into <= 4 chunks; after a chunk's heads are attended
+    # (one launch per head), its all-gather runs on a communication stream while
+    # the next chunk computes -- only the last chunk's exchange is exposed.
+    # Chunk c gathers every rank's slots [cb[c], cb[c+1]) into fulls[c]
+    # ([world * slots][n][128], rank-major); `gathered_layer` reassembles the layer.
+    overlap = dist_on and world > 1
+    head_map = [(r, hl) for r in runs for hl in range(r["seg"].h1 - r["seg"].h0)]
+    nchunk = min(4, hmax)
+    cb = [hmax * i // nchunk for i in range(nchunk + 1)]
+    fulls = [torch.empty((world * (cb[i + 1] - cb[i]), n, 128), dtype=torch.bfloat16, device=dev)
+             for i in range(nchunk)] if overlap else None
+    comm = torch.cuda.Stream(device=dev) if overlap else None
+
+    def attend_head(j, outbuf, dense=False):
+        r, hl = head_map[j]
+        s_, f = r["seg"], r["fpl"]
+        gl = hl * (s_.g1 - s_.g0) // (s_.h1 - s_.h0)
+        args = (r["q"][hl: hl + 1], r["k"][gl: gl + 1], r["v"][gl: gl + 1],
+                outbuf[s_.h0 - h0 + hl: s_.h0 - h0 + hl + 1], 1, 1, n)
+        if dense:
+            fp.fp_dense_causal_attn(*args, ws=f.ws, ws_bytes=f.ws_bytes)
+        else:
+            fp.fp_sparse_attn(*args, f.row_ptr[hl: hl + 1], f.col_idx[hl: hl + 1], f.ws, f.ws_bytes)
+
+    def gather_overlapped(outbuf, dense=False):
+        for c in range(nchunk):
+            for j in range(cb[c], min(cb[c + 1], h1 - h0)):
+                attend_head(j, outbuf, dense)
+            e_c = torch.cuda.Event()
+            e_c.record(stream)
+            comm.wait_event(e_c)
+            with torch.cuda.stream(comm):
+                dist.all_gather_into_tensor(fulls[c], outbuf[cb[c]: cb[c + 1]])
+        stream.wait_stream(comm)
+
+    def gathered_layer():
+        """[H][n][128] from the chunked all-gather (N > 1, overlapped path)."""
+        parts = []
+        for r_ in range(world):
+            a_, b_ = fpdist.head_range(H, world, r_)
+            for j in range(b_ - a_):
+                c = max(i for i in range(nchunk) if cb[i] <= j)
+                parts.append(fulls[c][r_ * (cb[c + 1] - cb[c]) + j - cb[c]])
+        return torch.stack(parts)
+
     def step(rec=None, gamma=w.gamma):
         for r in runs:
             if rec is not None:
@@ -587,13 +634,25 @@ def main():
             r["fpl"].select(gamma, w.min_budget, with_stats=False)
             if rec is not None:
                 rec["a0"].append(ev()); rec["a0"][-1].record(stream)
-            r["fpl"].attn(r["q"], r["k"], r["v"], r["o"])
+            if not overlap:
+                r["fpl"].attn(r["q"], r["k"], r["v"], r["o"])
             if rec is not None:
                 rec["a1"].append(ev()); rec["a1"][-1].record(stream)
-        if dist_on:
+        if overlap:
+            # per-head attention + chunked all-gathers (stage events: the
+            # attention + exposed exchange land in the last run's a0..a1 span)
+            if rec is not None:
+                rec["a0"][-1] = ev(); rec["a0"][-1].record(stream)
+            gather_overlapped(out)
+            if rec is not None:
+                rec["a1"][-1] = ev(); rec["a1"][-1].record(stream)
+        elif dist_on:
             dist.all_gather_into_tensor(full, out)
 
     def dense_step():
+        if overlap:
+            gather_overlapped(out_dense, dense=True)
+            return
         for r in runs:
             r["fpl"].dense(r["q"], r["k"], r["v"], r["od"])
         if dist_on:
@@ -754,7 +813,7 @@ def main():
             ref = torch.empty_like(qf)
             fref = fp.FlexPrefill(H, G, n, device=dev)
             fref.layer(qf, kf, vf, ref, w.gamma, w.tau, w.min_budget)
-            got = fpdist.unpad_gathered(full, H, world)
+            got = gathered_layer() if overlap else fpdist.unpad_gathered(full, H, world)
             torch.cuda.synchronize()
             ok[0] = 1 if torch.equal(ref, got) else 0
             del qf, kf, vf, ref, fref, got
