@@ -99,6 +99,23 @@ def dense_flops(H, n, d=128):
     return H * 4 * d * n * (n + 1) // 2
 
 
+def stage_work(H, G, n, n_qa, b=128, d=128):
+    """Algorithmic work of stages (i) and (ii) per layer (SURVEY §8(d) per-unit
+    figures): plan = two representative passes (2 * 2 b n d FLOP per head; K
+    read once per pass and KV group, Q^ per head, a_v / a_s written, Q of the
+    Query-Aware heads read once for Q_bar, A_bar written); select = the top-mass
+    scores read once per radix pass (3) and once by the compaction, plus the
+    CSR written."""
+    nb = -(-n // b)
+    tri = nb * (nb + 1) // 2
+    plan_flops = H * 2 * (2 * b * n * d)
+    plan_bytes = (2 * G * n * d * 2 + H * b * d * 2 * 2 + H * n * 8
+                  + n_qa * n * d * 2 + n_qa * tri * 4)
+    seg = (H - n_qa) * 2 * n + n_qa * tri
+    sel_bytes = seg * 4 * 4 + H * (nb + 1) * 4 + H * tri * 4 * 0.3
+    return plan_flops, plan_bytes, sel_bytes
+
+
 # ------------------------------------------------------------------ clocks ---
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -822,6 +839,16 @@ def main():
 
     # ---- roofline of the dominant kernel (fp_sparse_attn), from the same timed pass
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+    # stages (i) / (ii) against the HBM copy peak (and the plan's exp / MMA work)
+    pf, pb, sb = stage_work(h1 - h0, g_hi - g_lo, n, int(np.sum(patterns)))
+    hbm = peaks.get("hbm_gbs", 6546.0)
+    stage_roofline = {
+        "plan": {"algorithmic_bytes": pb, "GB_s": pb / (plan_ms / 1e3) / 1e9,
+                 "frac_of_hbm": pb / (plan_ms / 1e3) / 1e9 / hbm, "tflops": pf / (plan_ms / 1e3) / 1e12,
+                 "exp2_per_s": pf / (2 * 128) / (plan_ms / 1e3)},
+        "select": {"algorithmic_bytes": sb, "GB_s": sb / (sel_ms / 1e3) / 1e9,
+                   "frac_of_hbm": sb / (sel_ms / 1e3) / 1e9 / hbm},
+        "note": "bench.stage_work(): per-unit bytes / FLOP of SURVEY §8(d); peak = MEASURED_PEAKS.json hbm_gbs"}
     peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
     peak_burst = peaks.get("bf16_tflops", 1590.0)
     achieved = f_useful / (attn_ms / 1e3) / 1e12  # this rank's heads / this rank's attn time
@@ -863,6 +890,7 @@ def main():
             "latency_ms_per_layer": ms_step,
             "ms_per_step_cuda_graph": graph_ms,
             "ms_per_step_median": float(np.median(ms_list)), "ms_per_step_min": float(np.min(ms_list)),
+            "stage_roofline": stage_roofline,
             "stage_ms": {"plan": plan_ms, "select": sel_ms, "attn": attn_ms,
                          "note": "per-stage CUDA events inside the same timed steps as ms_per_step"
                                  + ("; rank 0's heads" if dist_on else "")},
