@@ -138,6 +138,11 @@ fp_status fp_layout_bshd(int batch, int heads, int kv_heads, int seq_len, fp_lay
 typedef struct {
   const float *a_v, *a_s, *a_hat, *a_bar, *k_bar, *q_bar, *A_bar, *As;
   const int32_t *sel_v, *sel_s, *sel_qa, *sel_count, *row_nnz_pre;
+  /* attention scheduler of the last fp_sparse_attn / fp_dense_causal_attn with
+   * this ws (int32 [2]): [0] work counter, [1] number of work items (head,
+   * query-block pair) that were redone with a row-max pass on every tile
+   * because a score exceeded its row's reference by more than 64 (log2) */
+  const int32_t *attn_sched;
 } fp_debug_ptrs;
 
 /* Bytes of device workspace needed by fp_plan/fp_select/fp_sparse_attn for

@@ -63,7 +63,7 @@ class Layout(ctypes.Structure):
 class DebugPtrs(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "a_v", "a_s", "a_hat", "a_bar", "k_bar", "q_bar", "A_bar", "As",
-        "sel_v", "sel_s", "sel_qa", "sel_count", "row_nnz_pre")]
+        "sel_v", "sel_s", "sel_qa", "sel_count", "row_nnz_pre", "attn_sched")]
 
 
 _lib = None
@@ -374,4 +374,5 @@ class FlexPrefill:
             sel_qa=view(d.sel_qa, H * tri, i32, (H, tri)),
             sel_count=view(d.sel_count, H * 4, i32, (H, 4)),
             row_nnz_pre=view(d.row_nnz_pre, H * nb, i32, (H, nb)),
+            attn_sched=view(d.attn_sched, 2, i32, (2,)),
         )

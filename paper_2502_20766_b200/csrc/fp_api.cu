@@ -459,6 +459,7 @@ fp_status fp_debug_view(const void* ws, int heads, int kv_heads, int seq_len, in
   out->sel_qa = wsp<int32_t>(w, L.sel_qa);
   out->sel_count = wsp<int32_t>(w, L.sel_count);
   out->row_nnz_pre = wsp<int32_t>(w, L.row_nnz_pre);
+  out->attn_sched = wsp<int32_t>(w, L.sched);
   return FP_OK;
 }
 

@@ -10,7 +10,7 @@ namespace fp {
 cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
-                           const void* const* peer_o, int n_peer, int* work_counter, cudaStream_t st);
+                           const void* const* peer_o, int n_peer, int* sched, cudaStream_t st);
 cudaError_t launch_attn_b64(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                             const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                             const int32_t* row_ptr, const int32_t* col_idx, cudaStream_t st);
@@ -26,9 +26,10 @@ cudaError_t launch_attn(const Shape& s, const WsLayout& L, void* ws, const Layou
     return launch_attn_b64(s, lay, qmap, kmap, vmap, o, row_ptr, col_idx, st);
   }
   const Shape s128 = s.b == 128 ? s : make_shape(s.H, s.G, s.n, 128);
-  // work counter of the persistent scheduler (ws is optional scratch)
-  int* counter = ws ? wsp<int>(ws, L.sched) : nullptr;
-  return launch_attn_v8(s128, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, peer_o, n_peer, counter, st);
+  // persistent scheduler scratch (ws is optional: without it the exact kernel
+  // runs one CTA per work item)
+  int* sched = ws ? wsp<int>(ws, L.sched) : nullptr;
+  return launch_attn_v8(s128, lay, qmap, kmap, vmap, o, row_ptr, col_idx, dense, peer_o, n_peer, sched, st);
 }
 
 }  // namespace fp

@@ -64,15 +64,13 @@ constexpr int kThreads8 = 384;
 constexpr int kKS8 = 2, kVS8 = 3;  // K / V ring depths (tiles)
 constexpr uint32_t kColS8 = 0, kColO8 = 256;
 constexpr float kRescale8 = 8.0f;  // lazy rescale: tolerate P up to 2^8 (as v5)
-// exponentials per row and tile (of 128) computed on the FMA pipe instead of
-// the MUFU (16 ex2/clk/SM, the softmax floor: 1024 cycles per 128x128 tile).
-// Measured on B200 (tools/attn_ab2.py block timing, C3 gamma 0.95): 0 -> 34.3
-// ms, 16 -> 34.5, 32 -> 35.5 (dense: 115.4 -> 120.9 at 32): under the 1 kW
-// power cap the extra FMA-pipe work lowers the clock more than it saves.
-#ifndef FP_EMU8
-#define FP_EMU8 0
-#endif
-constexpr int kEmu8 = FP_EMU8;
+// a tile row sum above 2^64 (some P beyond 2^64 against the row's reference)
+// flags the work item for an exact (max-first) redo
+constexpr float kGuard8 = 18446744073709551616.0f;
+// FMA-pipe exp2 (FlashAttention-4's MUFU offload, 16 or 32 of each row's 128
+// exponentials per tile) was measured slower on every v8 variant (C3 gamma
+// 0.95: 32.2 -> 34.9 / 38.0 ms; dense 112.5 -> 122.5 / 130.3 ms,
+// profiles/r02_attn_nomax.txt) and is not built.
 // P handed to the tensor core in two halves (keys 0-63, 64-127): the softmax
 // stores P in 32-key chunks as the exponentials finish (tcgen05.st overlaps
 // the next chunk's MUFU work) and arrives on p_lo once the first half is
@@ -100,7 +98,14 @@ struct Attn8Smem {
   uint64_t v_full[kVS8], v_empty[kVS8];
   uint64_t s_full[2], p_full[2], p_lo[2], pv_done[2];
   uint32_t tmem_base;
+  // exact redo of flagged work items (see the fetcher): ring written by the
+  // softmax warps, read by the fetcher; per-item dedupe flags; completed
+  // softmax-warp items (8 per item)
+  int redo[8];
+  int redo_tail, done_warps;
+  unsigned redo_flag[8];
 };
+constexpr int kExact8 = 1 << 30;  // item id bit: recompute max-first on every tile
 
 FP_DEV float fmax3_8(float a, float b, float c) {
   float d;
@@ -120,32 +125,6 @@ FP_DEV void fadd2_8(float& d0, float& d1, float a0, float a1, float b0, float b1
       "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
       : "=f"(d0), "=f"(d1)
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-FP_DEV void ffma2v_8(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
-  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-}
-// 2^x for a pair on the FMA/ALU pipes (FlashAttention-4's MUFU offload):
-// x = j + f (j = rint(x), |f| <= 1/2), 2^f by a degree-3 minimax polynomial
-// (max rel. error 7.5e-5; P is rounded to bf16 afterwards, 2^-9), 2^j added
-// into the exponent field. x is clamped at -125 (masked keys are zeroed
-// separately on the diagonal block).
-FP_DEV void exp2_emu2_8(float x0, float x1, float& y0, float& y1) {
-  const float kMagic = 12582912.0f;  // 1.5 * 2^23: rounds to an integer in the low mantissa bits
-  x0 = fmaxf(x0, -125.0f);
-  x1 = fmaxf(x1, -125.0f);
-  float t0, t1, j0, j1, f0, f1, p0, p1;
-  fadd2_8(t0, t1, x0, x1, kMagic, kMagic);
-  fadd2_8(j0, j1, t0, t1, -kMagic, -kMagic);
-  fadd2_8(f0, f1, x0, x1, -j0, -j1);
-  ffma2_8(p0, p1, f0, f1, 0.0551716626f, 0.242611155f);
-  ffma2v_8(p0, p1, p0, p1, f0, f1, 0.69326099f, 0.69326099f);
-  ffma2v_8(p0, p1, p0, p1, f0, f1, 0.999928072f, 0.999928072f);
-  y0 = __uint_as_float(__float_as_uint(t0) * 8388608u + __float_as_uint(p0));
-  y1 = __uint_as_float(__float_as_uint(t1) * 8388608u + __float_as_uint(p1));
 }
 FP_DEV void tmem_ld_32x32b_x64_8(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 " FP_REGLIST64 ", [%64];"
@@ -340,6 +319,14 @@ FP_DEV Item decode_item(int item, int H, int G, int nb, long long cap, const int
 // first S MMAs run while the softmax warpgroups finish the current item, and
 // a row's O is overwritten (first PV, accumulate = 0) only after its P -- which
 // the warpgroup produces after its previous epilogue read O -- is stored.
+// Softmax without a per-tile row-max pass (see the softmax warps): a row whose
+// scores later exceed its reference by > 64 (log2) is flagged; its work item
+// is pushed onto a CTA-local redo ring and the fetcher re-publishes it with
+// kExact8 (every tile max-first) before taking new work, and before exiting
+// waits until every published item has finished (done_warps) so late flags
+// are still redone. The redo overwrites the item's output rows. sched
+// (optional workspace scratch, zeroed before the launch): [0] work counter,
+// [1] number of redone items (diagnostics).
 template <bool DENSE>
 __global__ void __launch_bounds__(kThreads8, 1)
     attn8_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
@@ -347,7 +334,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
                  const TLayout ol, int Hp, int Gp, int H, int G, int n, int nb, long long cap,
                  const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                  float scale_log2, const unsigned long long* __restrict__ peer_o, int n_peer,
-                 int total_items, int* __restrict__ work_counter) {
+                 int total_items, int* __restrict__ sched) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 tiles need 1024-B alignment
   Attn8Smem& sm = *reinterpret_cast<Attn8Smem*>(smem_raw);
@@ -381,6 +368,8 @@ __global__ void __launch_bounds__(kThreads8, 1)
       mbar_init(&sm.pv_done[x], 1);
     }
     mbar_fence_init();
+    sm.redo_tail = sm.done_warps = 0;
+    for (int i = 0; i < 8; ++i) sm.redo_flag[i] = 0, sm.redo[i] = -1;
   }
   tc_fence_before();
   __syncthreads();
@@ -411,13 +400,44 @@ __global__ void __launch_bounds__(kThreads8, 1)
         uint64_t* empty = isK ? sm.k_empty : sm.v_empty;
         const CUtensorMap* map = isK ? &kmap : &vmap;
         int e = 0;  // union entries loaded so far (all items)
+        int redo_head = 0, n_new = 0;
+        bool drained = false;
         for (int k = 0;; ++k) {
           int item;
           if (isK) {
-            // scheduler: fetch the k-th item and publish it
-            item = work_counter ? atomicAdd(work_counter, 1) : (int)blockIdx.x + k * (int)gridDim.x;
-            if (item >= total_items) item = -1;
+            // scheduler: the k-th item of this CTA -- a flagged item to redo
+            // first, else new work; when new work has run out, wait until all
+            // published items finished (their flags are in) and exit when no
+            // redo is pending
+            volatile int* vtail = &sm.redo_tail;
+            volatile int* vdone = &sm.done_warps;
+            for (;;) {
+              if (redo_head < *vtail) {
+                // the pusher reserves its slot (tail) before writing it: wait
+                // for the entry, then free the slot (-1)
+                volatile int* slot = &sm.redo[redo_head++ & 7];
+                while ((item = *slot) < 0) __nanosleep(32);
+                *slot = -1;
+                item |= kExact8;
+                if (sched) atomicAdd(sched + 1, 1);
+                break;
+              }
+              if (!drained) {
+                item = sched ? atomicAdd(sched, 1) : (int)blockIdx.x + n_new * (int)gridDim.x;
+                ++n_new;
+                if (item < total_items) break;
+                drained = true;
+              }
+              if (*vdone == 8 * k) {
+                __threadfence_block();
+                if (redo_head < *vtail) continue;
+                item = -1;
+                break;
+              }
+              __nanosleep(64);
+            }
             if (k >= 2) mbar_wait(&sm.item_empty[k & 1], ((k - 2) >> 1) & 1);
+            sm.redo_flag[k & 7] = 0;
             sm.item[k & 1] = item;
             mbar_arrive(&sm.item_full[k & 1]);
           } else {
@@ -426,7 +446,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
             mbar_arrive(&sm.item_empty[k & 1]);
           }
           if (item < 0) break;
-          const Item it = decode_item<DENSE>(item, H, G, nb, cap, row_ptr, col_idx);
+          const Item it = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx);
           if (isK) {
             // Q_A, Q_B of this item once the previous item's S MMAs are done
             if (k >= 1) mbar_wait(&sm.q_empty, (k - 1) & 1);
@@ -441,6 +461,14 @@ __global__ void __launch_bounds__(kThreads8, 1)
             const int kb = un.next(mask);
             const int s = e % depth;
             if (e >= depth) mbar_wait(&empty[s], ((e - depth) / depth) & 1);
+#ifdef FP_XNOTMA8
+            // experiment: after the ring's first fill, reuse the stale tiles
+            // (measures the kernel without L2 -> smem traffic; wrong results)
+            if (e >= depth) {
+              mbar_arrive(&full[s]);
+              continue;
+            }
+#endif
             mbar_arrive_expect_tx(&full[s], kTileBytes);
             tma_tile_hint(isK ? sm.k[s] : sm.v[s], map, &full[s], kb * 128, it.g, Gp, pol);
           }
@@ -463,7 +491,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
           __syncwarp();
           if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
           if (item < 0) break;
-          const Item itm = decode_item<DENSE>(item, H, G, nb, cap, row_ptr, col_idx);
+          const Item itm = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx);
           int pend[2] = {-1, -1};  // union entry of X's S awaiting its PV
           int lcnt[2] = {0, 0};    // S tiles issued per stream in this item
           auto issue_pv = [&](int x) {
@@ -552,10 +580,12 @@ __global__ void __launch_bounds__(kThreads8, 1)
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
       if (item < 0) break;
-      const Item itm = decode_item<DENSE>(item, H, G, nb, cap, row_ptr, col_idx);
+      const Item itm = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx);
+      const bool exact = (item & kExact8) != 0;
       const int nX = x ? itm.nB : itm.nA;
       const int qb = x ? itm.qbB : itm.qbA;
-      float m_used = -INFINITY, l = 0.f;
+      float m_used = -INFINITY, l = 0.f;  // P = 2^(s * scale - m_used), l = sum of P
+      bool bad = false;                   // this row needs the exact redo
       for (int t = 0; t < nX; ++t) {
         const int ph = (T + t) & 1;  // this tile's phase of s_full / p_lo / p_full
         FP_T8(6);
@@ -570,45 +600,34 @@ __global__ void __launch_bounds__(kThreads8, 1)
 #endif
         tc_fence_after();
         float v[128];
-        tmem_ld_32x32b_x64_8(tS, reinterpret_cast<uint32_t*>(v));
-        tmem_ld_32x32b_x64_8(tS + 64, reinterpret_cast<uint32_t*>(v + 64));
-        // probe pv_done(t - 1) now (complete: S(t) followed PV(t - 1) in the
-        // in-order MMA stream) so the probe's latency overlaps the TMEM load;
-        // the phase is still consumed below, the loop only runs if it failed
-        const bool pv_ok = t == 0 || mbar_try_wait(smem_u32(&sm.pv_done[x]), (T + t - 1) & 1);
-        tmem_wait_ld();
-        FP_T8(1);
-        if (t == nX - 1) {  // the diagonal block: keys j <= r only
+        auto load_s = [&]() {
+          tmem_ld_32x32b_x64_8(tS, reinterpret_cast<uint32_t*>(v));
+          tmem_ld_32x32b_x64_8(tS + 64, reinterpret_cast<uint32_t*>(v + 64));
+        };
+        auto mask_diag = [&]() {
+          if (t == nX - 1) {  // the diagonal block: keys j <= r only
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
-            if (c > r) v[c] = -INFINITY;
-        }
-        // row max: 8 independent fmax3 chains (8 x 16 columns), then a tree
-        float mc[8];
+            for (int c = 0; c < 128; ++c)
+              if (c > r) v[c] = -INFINITY;
+          }
+        };
+        // row max of the raw scores (log2 domain): 8 independent fmax3 chains
+        // (8 x 16 columns), then a tree
+        auto row_max = [&]() {
+          float mc[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(v[16 * j], v[16 * j + 1], v[16 * j + 2]);
+          for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(v[16 * j], v[16 * j + 1], v[16 * j + 2]);
 #pragma unroll
-        for (int c = 3; c < 15; c += 2)
+          for (int c = 3; c < 15; c += 2)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(mc[j], v[16 * j + c], v[16 * j + c + 1]);
+            for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(mc[j], v[16 * j + c], v[16 * j + c + 1]);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) mc[j] = fmaxf(mc[j], v[16 * j + 15]);
-        const float mx = fmaxf(fmax3_8(mc[0], mc[1], mc[2]), fmax3_8(mc[3], mc[4], fmax3_8(mc[5], mc[6], mc[7]))) *
-                         scale_log2;
-        float alpha = 1.f;
-        if (mx > m_used + kRescale8) {
-          alpha = exp2f(m_used - mx);  // 0 on the first tile
-          m_used = mx;
-        }
-        const float nm = -m_used;
-        FP_T8(2);
-        // O_X holds sum_{earlier} P V: PV of the previous tile completed before
-        // S of this one (one in-order tcgen05.mma stream), so O can be
-        // rescaled now, before PV's first half is released. Every pv_done
-        // phase is consumed (here, normally long complete; an unconsumed phase
-        // is what compute-sanitizer synccheck reports).
-        if (!pv_ok) mbar_wait(&sm.pv_done[x], (T + t - 1) & 1);
-        if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          for (int j = 0; j < 8; ++j) mc[j] = fmaxf(mc[j], v[16 * j + 15]);
+          return fmaxf(fmax3_8(mc[0], mc[1], mc[2]), fmax3_8(mc[3], mc[4], fmax3_8(mc[5], mc[6], mc[7]))) *
+                 scale_log2;
+        };
+        // O_X *= alpha (per lane) once PV of the previous tile is complete
+        auto rescale_o = [&](float alpha) {
           tc_fence_after();
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -619,45 +638,83 @@ __global__ void __launch_bounds__(kThreads8, 1)
             for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
             tmem_st32(tO + q4 * 32, ov);
           }
-        }
-        FP_T8(3);
+        };
+        // exponentials of chunk ch (32 keys) against -nm in place, row-sum
+        // partials, packed to bf16 pairs
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
+        auto exp_chunk = [&](int ch, float nm, uint32_t* pk) {
           const int c0 = ch * 32;
 #pragma unroll
           for (int c = c0; c < c0 + 32; c += 2) ffma2_8(v[c], v[c + 1], v[c], v[c + 1], scale_log2, nm);
 #pragma unroll
-          for (int c = c0; c < c0 + 32; ++c)
-            if (c < 128 - kEmu8) v[c] = fast_exp2(v[c]);
-#pragma unroll
-          for (int c = c0; c < c0 + 32; c += 2)
-            if (c >= 128 - kEmu8) exp2_emu2_8(v[c], v[c + 1], v[c], v[c + 1]);
-          if (kEmu8 > 0 && t == nX - 1) {
-#pragma unroll
-            for (int c = c0; c < c0 + 32; ++c)
-              if (c >= 128 - kEmu8 && c > r) v[c] = 0.f;
-          }
+          for (int c = c0; c < c0 + 32; ++c) v[c] = fast_exp2(v[c]);
 #pragma unroll
           for (int c = c0; c < c0 + 32; c += 4) {
             fadd2_8(s0, s1, s0, s1, v[c], v[c + 1]);
             fadd2_8(s2, s3, s2, s3, v[c + 2], v[c + 3]);
           }
-          uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) pk[c] = pack_bf16x2(v[c0 + 2 * c], v[c0 + 2 * c + 1]);
-          // p_lo after chunk 2's exponentials: the stores of chunks 0-1 have
-          // completed by then, so the wait does not stall the MUFU stream
-          if (ch == 2) {
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive(&sm.p_lo[x]);
-            FP_T8(4);
+        };
+        // p_lo after chunk 2's exponentials: the stores of chunks 0-1 have
+        // completed by then, so the wait does not stall the MUFU stream
+        auto release_lo = [&]() {
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&sm.p_lo[x]);
+        };
+        load_s();
+        // probe pv_done(t - 1) now (complete: S(t) followed PV(t - 1) in the
+        // in-order MMA stream) so the probe's latency overlaps the TMEM load;
+        // the phase is still consumed below, the loop only runs if it failed
+        const bool pv_ok = t == 0 || mbar_try_wait(smem_u32(&sm.pv_done[x]), (T + t - 1) & 1);
+        tmem_wait_ld();
+        FP_T8(1);
+        mask_diag();
+        if (!pv_ok) mbar_wait(&sm.pv_done[x], (T + t - 1) & 1);
+        if (t > 0 && !exact) {
+          // Tiles after a row's first: no row-max pass (64 fmax3
+          // per row and tile plus the rescale vote; removing it measured -7%
+          // on C3, and every variant that kept a per-tile check inside the
+          // exponential stream -- the max under the exponentials, guards on
+          // partial sums -- lost the gain: profiles/r02_attn_nomax.txt).
+          // P = 2^(s * scale - m_used) against the reference fixed by the
+          // row's first tile (exact softmax up to rounding for any reference);
+          // the only hazard -- a later score > 64 above it (log2), P near
+          // fp32 overflow -- is flagged per lane from the tile's row sum and
+          // the whole work item is redone max-first (kExact8) by this CTA.
+          const float nm = -m_used;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t pk[16];
+            exp_chunk(ch, nm, pk);
+            if (ch == 2) release_lo();
+            tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
           }
-          tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
+          const float ts = (s0 + s1) + (s2 + s3);
+          bad |= !(ts <= kGuard8);
+          l += ts;
+        } else {
+          // max-first: a row's first tile, and every tile of a redone item;
+          // the reference moves to the max if it grew by > 2^8
+          const float mx = row_max();
+          float alpha = 1.f;
+          if (mx > m_used + kRescale8) {
+            alpha = exp2f(m_used - mx);  // 0 on the first tile
+            m_used = mx;
+          }
+          if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) rescale_o(alpha);
+          const float nm = -m_used;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            uint32_t pk[16];
+            exp_chunk(ch, nm, pk);
+            if (ch == 2) release_lo();
+            tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
+          }
+          l = l * alpha + ((s0 + s1) + (s2 + s3));
         }
-        l = l * alpha + ((s0 + s1) + (s2 + s3));
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -703,6 +760,16 @@ __global__ void __launch_bounds__(kThreads8, 1)
         tc_fence_before();  // O reads complete before P of the next item is released
       }
       T += nX;
+      // a row with an overflow hazard puts its item on the redo ring (once per
+      // item: the flag of its slot dedupes the warps / rows that flag it),
+      // then the warp reports the item done
+      const bool flag = __any_sync(0xffffffffu, bad);
+      if (lane_id() == 0) {
+        if (flag && atomicOr(&sm.redo_flag[k & 7], 1u) == 0)
+          *reinterpret_cast<volatile int*>(&sm.redo[atomicAdd(&sm.redo_tail, 1) & 7]) = item & ~kExact8;
+        __threadfence_block();
+        atomicAdd(&sm.done_warps, 1);
+      }
     }
     FP_T8_FLUSH(0, 8);
 #ifdef FP_TIMING
@@ -732,7 +799,7 @@ extern "C" int fp_debug_attn8_timing(unsigned long long* out, int reset) {
 cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
                            const int32_t* row_ptr, const int32_t* col_idx, bool dense,
-                           const void* const* peer_o, int n_peer, int* work_counter, cudaStream_t st) {
+                           const void* const* peer_o, int n_peer, int* sched, cudaStream_t st) {
   const size_t smem = attn8_smem_bytes();
   cudaError_t ea = ensure_smem_attr((const void*)attn8_kernel<true>, smem);
   if (ea == cudaSuccess) ea = ensure_smem_attr((const void*)attn8_kernel<false>, smem);
@@ -742,26 +809,23 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
   const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
   const int total = s.H * ((s.nb + 1) / 2);
   // persistent (one CTA per SM, dynamic work fetch) when a workspace holds the
-  // work counter; otherwise one CTA per item (a static round-robin over a
+  // scheduler; otherwise one CTA per item (a static round-robin over a
   // persistent grid would leave the per-item cost variance unbalanced)
-  const dim3 grid(work_counter ? std::min(total, nsm) : total);
-  if (work_counter) {
-    const cudaError_t em = cudaMemsetAsync(work_counter, 0, sizeof(int), st);
+  const dim3 grid(sched ? std::min(total, nsm) : total);
+  if (sched) {
+    const cudaError_t em = cudaMemsetAsync(sched, 0, 2 * sizeof(int), st);
     if (em != cudaSuccess) return em;
   }
   auto* op = reinterpret_cast<__nv_bfloat16*>(o);
+  const auto* po = reinterpret_cast<const unsigned long long*>(peer_o);
   if (dense)
-    attn8_kernel<true><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
-                                                      lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
-                                                      row_ptr, col_idx, scale_log2,
-                                                      reinterpret_cast<const unsigned long long*>(peer_o),
-                                                      n_peer, total, work_counter);
+    attn8_kernel<true><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per, s.H,
+                                                      s.G, s.n, s.nb, s.tri, row_ptr, col_idx, scale_log2,
+                                                      po, n_peer, total, sched);
   else
-    attn8_kernel<false><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per,
-                                                       lay.k.per, s.H, s.G, s.n, s.nb, s.tri,
-                                                       row_ptr, col_idx, scale_log2,
-                                                       reinterpret_cast<const unsigned long long*>(peer_o),
-                                                       n_peer, total, work_counter);
+    attn8_kernel<false><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per,
+                                                       s.H, s.G, s.n, s.nb, s.tri, row_ptr, col_idx,
+                                                       scale_log2, po, n_peer, total, sched);
   return cudaGetLastError();
 }
 

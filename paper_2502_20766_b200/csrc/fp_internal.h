@@ -65,7 +65,7 @@ struct WsLayout {
   size_t budget_added;       // int32 [H][nb]
   size_t budget_removed;     // int32 [H][nb]
   size_t selbits;            // uint32 [H][nb][nbw] per-row QA selection (qa_mode 1)
-  size_t sched;              // int32 [64] scheduler scratch
+  size_t sched;              // int32 [64] attention scheduler: [0] work counter, [1] redone items
   size_t total;
   int nbw;                   // words per bitmap row
 };
