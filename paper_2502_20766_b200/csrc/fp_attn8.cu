@@ -64,7 +64,7 @@ constexpr int kThreads8 = 384;
 constexpr int kKS8 = 2, kVS8 = 3;  // K / V ring depths (tiles)
 constexpr uint32_t kColS8 = 0, kColO8 = 256;
 constexpr float kRescale8 = 8.0f;  // lazy rescale: tolerate P up to 2^8 (as v5)
-// a tile row sum above 2^64 (some P beyond 2^64 against the row's reference)
+// a row sum above 2^64 (some P may exceed 2^64 against the row's reference)
 // flags the work item for an exact (max-first) redo
 constexpr float kGuard8 = 18446744073709551616.0f;
 // FMA-pipe exp2 (FlashAttention-4's MUFU offload, 16 or 32 of each row's 128
@@ -584,8 +584,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
       const bool exact = (item & kExact8) != 0;
       const int nX = x ? itm.nB : itm.nA;
       const int qb = x ? itm.qbB : itm.qbA;
-      float m_used = -INFINITY, l = 0.f;  // P = 2^(s * scale - m_used), l = sum of P
-      bool bad = false;                   // this row needs the exact redo
+      float m_used = -INFINITY, l = 0.f;  // P = 2^(s * scale - m_used), l = sum of this thread's P
       for (int t = 0; t < nX; ++t) {
         const int ph = (T + t) & 1;  // this tile's phase of s_full / p_lo / p_full
         FP_T8(6);
@@ -600,49 +599,71 @@ __global__ void __launch_bounds__(kThreads8, 1)
 #endif
         tc_fence_after();
         float v[128];
-        auto load_s = [&]() {
-          tmem_ld_32x32b_x64_8(tS, reinterpret_cast<uint32_t*>(v));
-          tmem_ld_32x32b_x64_8(tS + 64, reinterpret_cast<uint32_t*>(v + 64));
-        };
-        auto mask_diag = [&]() {
-          if (t == nX - 1) {  // the diagonal block: keys j <= r only
+        tmem_ld_32x32b_x64_8(tS, reinterpret_cast<uint32_t*>(v));
+        tmem_ld_32x32b_x64_8(tS + 64, reinterpret_cast<uint32_t*>(v + 64));
+        // probe pv_done(t - 1) now (complete: S(t) followed PV(t - 1) in the
+        // in-order MMA stream) so the probe's latency overlaps the TMEM load;
+        // the phase is still consumed below, the loop only runs if it failed
+        const bool pv_ok = t == 0 || mbar_try_wait(smem_u32(&sm.pv_done[x]), (T + t - 1) & 1);
+        tmem_wait_ld();
+        FP_T8(1);
+        if (t == nX - 1) {  // the diagonal block: keys j <= r only
 #pragma unroll
-            for (int c = 0; c < 128; ++c)
-              if (c > r) v[c] = -INFINITY;
-          }
-        };
-        // row max of the raw scores (log2 domain): 8 independent fmax3 chains
-        // (8 x 16 columns), then a tree
-        auto row_max = [&]() {
+          for (int c = 0; c < 128; ++c)
+            if (c > r) v[c] = -INFINITY;
+        }
+        if (!pv_ok) mbar_wait(&sm.pv_done[x], (T + t - 1) & 1);
+        // Tiles after a row's first: no row-max pass (64 fmax3 per row and
+        // tile plus the rescale vote; removing it measured -7% on C3, and every
+        // variant that kept a per-tile check inside the exponential stream --
+        // the max under the exponentials, guards on partial sums -- lost the
+        // gain: profiles/r02_attn_nomax.txt). P = 2^(s * scale - m_used)
+        // against the reference fixed by the row's first tile (exact softmax
+        // up to rounding for any reference); the only hazard -- a later score
+        // > 64 above it (log2), P near fp32 overflow -- is flagged per lane
+        // once per row from the row sum (l <= 2^64 bounds every P; a larger,
+        // infinite or NaN sum flags the row), and the whole work item is
+        // redone max-first (kExact8) by this CTA. Max-first: a row's first
+        // tile and every tile of a redone item; the reference moves to the
+        // max if it grew by > 2^8.
+        const bool fast = t > 0 && !exact;
+        float alpha = 1.f;
+        if (!fast) {
+          // row max of the raw scores: 8 independent fmax3 chains, then a tree
+          constexpr int kJ = 16;
           float mc[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(v[16 * j], v[16 * j + 1], v[16 * j + 2]);
+          for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(v[kJ * j], v[kJ * j + 1], v[kJ * j + 2]);
 #pragma unroll
-          for (int c = 3; c < 15; c += 2)
+          for (int c = 3; c + 1 < kJ; c += 2)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(mc[j], v[16 * j + c], v[16 * j + c + 1]);
+            for (int j = 0; j < 8; ++j) mc[j] = fmax3_8(mc[j], v[kJ * j + c], v[kJ * j + c + 1]);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) mc[j] = fmaxf(mc[j], v[16 * j + 15]);
-          return fmaxf(fmax3_8(mc[0], mc[1], mc[2]), fmax3_8(mc[3], mc[4], fmax3_8(mc[5], mc[6], mc[7]))) *
-                 scale_log2;
-        };
-        // O_X *= alpha (per lane) once PV of the previous tile is complete
-        auto rescale_o = [&](float alpha) {
-          tc_fence_after();
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            uint32_t ov[32];
-            tmem_ld32(tO + q4 * 32, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
-            tmem_st32(tO + q4 * 32, ov);
+          for (int j = 0; j < 8; ++j) mc[j] = fmaxf(mc[j], v[kJ * j + kJ - 1]);
+          const float mx =
+              fmaxf(fmax3_8(mc[0], mc[1], mc[2]), fmax3_8(mc[3], mc[4], fmax3_8(mc[5], mc[6], mc[7]))) * scale_log2;
+          if (mx > m_used + kRescale8) {
+            alpha = exp2f(m_used - mx);  // 0 on the first tile
+            m_used = mx;
           }
-        };
-        // exponentials of chunk ch (32 keys) against -nm in place, row-sum
-        // partials, packed to bf16 pairs
+          if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+            // O_X holds sum_{earlier} P V (PV(t - 1) is complete): rescale
+            tc_fence_after();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t ov[32];
+              tmem_ld32(tO + q * 32, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
+              tmem_st32(tO + q * 32, ov);
+            }
+          }
+        }
+        const float nm = -m_used;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        auto exp_chunk = [&](int ch, float nm, uint32_t* pk) {
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
           const int c0 = ch * 32;
 #pragma unroll
           for (int c = c0; c < c0 + 32; c += 2) ffma2_8(v[c], v[c + 1], v[c], v[c + 1], scale_log2, nm);
@@ -653,77 +674,33 @@ __global__ void __launch_bounds__(kThreads8, 1)
             fadd2_8(s0, s1, s0, s1, v[c], v[c + 1]);
             fadd2_8(s2, s3, s2, s3, v[c + 2], v[c + 3]);
           }
+          uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) pk[c] = pack_bf16x2(v[c0 + 2 * c], v[c0 + 2 * c + 1]);
-        };
-        // p_lo after chunk 2's exponentials: the stores of chunks 0-1 have
-        // completed by then, so the wait does not stall the MUFU stream
-        auto release_lo = [&]() {
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane_id() == 0) mbar_arrive(&sm.p_lo[x]);
-        };
-        load_s();
-        // probe pv_done(t - 1) now (complete: S(t) followed PV(t - 1) in the
-        // in-order MMA stream) so the probe's latency overlaps the TMEM load;
-        // the phase is still consumed below, the loop only runs if it failed
-        const bool pv_ok = t == 0 || mbar_try_wait(smem_u32(&sm.pv_done[x]), (T + t - 1) & 1);
-        tmem_wait_ld();
-        FP_T8(1);
-        mask_diag();
-        if (!pv_ok) mbar_wait(&sm.pv_done[x], (T + t - 1) & 1);
-        if (t > 0 && !exact) {
-          // Tiles after a row's first: no row-max pass (64 fmax3
-          // per row and tile plus the rescale vote; removing it measured -7%
-          // on C3, and every variant that kept a per-tile check inside the
-          // exponential stream -- the max under the exponentials, guards on
-          // partial sums -- lost the gain: profiles/r02_attn_nomax.txt).
-          // P = 2^(s * scale - m_used) against the reference fixed by the
-          // row's first tile (exact softmax up to rounding for any reference);
-          // the only hazard -- a later score > 64 above it (log2), P near
-          // fp32 overflow -- is flagged per lane from the tile's row sum and
-          // the whole work item is redone max-first (kExact8) by this CTA.
-          const float nm = -m_used;
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            uint32_t pk[16];
-            exp_chunk(ch, nm, pk);
-            if (ch == 2) release_lo();
-            tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
+          if (ch == 2) {
+            // p_lo after chunk 2's exponentials: the stores of chunks 0-1 have
+            // completed by then, so the wait does not stall the MUFU stream
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&sm.p_lo[x]);
+            FP_T8(4);
           }
-          const float ts = (s0 + s1) + (s2 + s3);
-          bad |= !(ts <= kGuard8);
-          l += ts;
-        } else {
-          // max-first: a row's first tile, and every tile of a redone item;
-          // the reference moves to the max if it grew by > 2^8
-          const float mx = row_max();
-          float alpha = 1.f;
-          if (mx > m_used + kRescale8) {
-            alpha = exp2f(m_used - mx);  // 0 on the first tile
-            m_used = mx;
-          }
-          if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) rescale_o(alpha);
-          const float nm = -m_used;
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            uint32_t pk[16];
-            exp_chunk(ch, nm, pk);
-            if (ch == 2) release_lo();
-            tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
-          }
-          l = l * alpha + ((s0 + s1) + (s2 + s3));
+          tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
         }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&sm.p_full[x]);
+        // the row sum after P is handed over (off the PV's critical path)
+        l = fmaf(l, alpha, (s0 + s1) + (s2 + s3));
         FP_T8(5);
 #ifdef FP_TIMING
         ++tacc[15];
 #endif
       }
+      // overflow hazard of this row's P (checked on its row sum)
+      const bool flag = __any_sync(0xffffffffu, !exact && nX > 1 && !(l <= kGuard8));
       if (nX > 0) {
         // epilogue: O / l -> bf16 -> global (rows past n are not stored)
         mbar_wait(&sm.pv_done[x], (T + nX - 1) & 1);
@@ -760,10 +737,9 @@ __global__ void __launch_bounds__(kThreads8, 1)
         tc_fence_before();  // O reads complete before P of the next item is released
       }
       T += nX;
-      // a row with an overflow hazard puts its item on the redo ring (once per
-      // item: the flag of its slot dedupes the warps / rows that flag it),
-      // then the warp reports the item done
-      const bool flag = __any_sync(0xffffffffu, bad);
+      // a flagged item goes on the redo ring (once per item: the flag of its
+      // slot dedupes the warps / rows that flag it), then the warp reports
+      // the item done
       if (lane_id() == 0) {
         if (flag && atomicOr(&sm.redo_flag[k & 7], 1u) == 0)
           *reinterpret_cast<volatile int*>(&sm.redo[atomicAdd(&sm.redo_tail, 1) & 7]) = item & ~kExact8;
