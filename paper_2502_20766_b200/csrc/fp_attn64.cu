@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kThreads64, 1)
                   const TLayout ol, int Hp, int Gp, int H, int G, int n, int nb, int nt, long long cap,
                   const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                   float scale_log2) {
+  FP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023u) __trap();
   Attn64Smem& sm = *reinterpret_cast<Attn64Smem*>(smem_raw);
@@ -373,7 +374,7 @@ cudaError_t launch_attn_b64(const Shape& s, const Layout& lay, const CUtensorMap
   if (ea != cudaSuccess) return ea;
   const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
   const dim3 grid(s.H * s.nt);
-  attn64_kernel<<<grid, kThreads64, smem, st>>>(qmap, kmap, vmap, reinterpret_cast<__nv_bfloat16*>(o),
+  FP_LAUNCH(attn64_kernel, grid, kThreads64, smem, st, qmap, kmap, vmap, reinterpret_cast<__nv_bfloat16*>(o),
                                                 lay.o, lay.q.per, lay.k.per, s.H, s.G, s.n, s.nb, s.nt,
                                                 s.tri, row_ptr, col_idx, scale_log2);
   return cudaGetLastError();

@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
                  const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                  float scale_log2, const unsigned long long* __restrict__ peer_o, int n_peer,
                  int total_items, int* __restrict__ sched) {
+  FP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 tiles need 1024-B alignment
   Attn8Smem& sm = *reinterpret_cast<Attn8Smem*>(smem_raw);
@@ -741,9 +742,10 @@ __global__ void __launch_bounds__(kThreads8, 1)
       // slot dedupes the warps / rows that flag it), then the warp reports
       // the item done
       if (lane_id() == 0) {
-        if (flag && atomicOr(&sm.redo_flag[k & 7], 1u) == 0)
+        if (flag && atomicOr(&sm.redo_flag[k & 7], 1u) == 0) {
           *reinterpret_cast<volatile int*>(&sm.redo[atomicAdd(&sm.redo_tail, 1) & 7]) = item & ~kExact8;
-        __threadfence_block();
+          __threadfence_block();  // the ring entry before the done count (rare: no fence otherwise)
+        }
         atomicAdd(&sm.done_warps, 1);
       }
     }
@@ -795,11 +797,11 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
   auto* op = reinterpret_cast<__nv_bfloat16*>(o);
   const auto* po = reinterpret_cast<const unsigned long long*>(peer_o);
   if (dense)
-    attn8_kernel<true><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per, s.H,
+    FP_LAUNCH(attn8_kernel<true>, grid, kThreads8, smem, st, qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per, s.H,
                                                       s.G, s.n, s.nb, s.tri, row_ptr, col_idx, scale_log2,
                                                       po, n_peer, total, sched);
   else
-    attn8_kernel<false><<<grid, kThreads8, smem, st>>>(qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per,
+    FP_LAUNCH(attn8_kernel<false>, grid, kThreads8, smem, st, qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per,
                                                        s.H, s.G, s.n, s.nb, s.tri, row_ptr, col_idx,
                                                        scale_log2, po, n_peer, total, sched);
   return cudaGetLastError();

@@ -19,6 +19,18 @@ constexpr int kBoxBytes = kTileBytes / 2;            // one 128x64 TMA box (SW12
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ------------------------------------------------------------- basics ------
+// Programmatic dependent launch (every kernel of the library is launched with
+// the PDL attribute, FP_LAUNCH in fp_internal.h): a kernel waits for the
+// previous kernel of its stream to complete (and its memory to be visible)
+// before touching anything, then lets the next one start launching, so the
+// launch / ramp of kernel i+1 overlaps the tail of kernel i. Both are no-ops
+// for a launch without the attribute.
+#define FP_PDL_ENTRY()                                        \
+  do {                                                        \
+    asm volatile("griddepcontrol.wait;" ::: "memory");        \
+    asm volatile("griddepcontrol.launch_dependents;" :::);    \
+  } while (0)
+
 FP_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -1,5 +1,6 @@
 // fp_internal.h -- workspace layout and kernel launchers (host side).
 #pragma once
+#include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
@@ -160,6 +161,30 @@ int attn_kv_box_rows();
 // once per (kernel, device) under a mutex (thread-safe; several GPUs driven
 // from one process each get their own setting) and returns its error.
 cudaError_t ensure_smem_attr(const void* fn, size_t bytes);
+
+// Kernel launch with programmatic stream serialization (PDL, see
+// FP_PDL_ENTRY): build with -DFP_NO_PDL for plain stream-ordered launches.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+#ifdef FP_NO_PDL
+  at[0].val.programmaticStreamSerializationAllowed = 0;
+#else
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+#endif
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+#define FP_LAUNCH(kern, grid, block, smem, st, ...) \
+  ::fp::launch_pdl(kern, dim3(grid), dim3(block), (size_t)(smem), st, __VA_ARGS__)
 
 // ---- launchers (return cudaGetLastError of their launches) ----
 cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void* q, const void* k,

@@ -90,6 +90,7 @@ __device__ float block_max(float v, float* red) {
 __global__ void rep_stats(int nchunks, int r_lo, const float* __restrict__ m_part,
                           const float* __restrict__ l_part, float* __restrict__ m_row,
                           float* __restrict__ mp_row) {
+  FP_PDL_ENTRY();
   const int h = blockIdx.x, r = threadIdx.x;
   const float* mp = m_part + (size_t)h * nchunks * 128 + r;
   const float* lp = l_part + (size_t)h * nchunks * 128 + r;
@@ -104,6 +105,7 @@ __global__ void rep_stats(int nchunks, int r_lo, const float* __restrict__ m_par
 // a_s[o] = (sum of the overlapping per-tile diagonal partials) / b  (A9)
 __global__ void slash_combine(int n, int nt, float inv_b, const float* __restrict__ as_part,
                               float* __restrict__ a_s) {
+  FP_PDL_ENTRY();
   const int h = blockIdx.y;
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= n) return;
@@ -123,6 +125,7 @@ __global__ void slash_combine(int n, int nt, float inv_b, const float* __restric
 __global__ void block_sums(int n, int nb, int b, const float* __restrict__ a_v,
                            const float* __restrict__ a_s, float* __restrict__ a_hat,
                            float* __restrict__ As) {
+  FP_PDL_ENTRY();
   __shared__ float red[33];
   const int kb = blockIdx.x, h = blockIdx.y;
   const size_t i = (size_t)h * n + (size_t)kb * b + threadIdx.x;
@@ -145,6 +148,7 @@ __global__ void __launch_bounds__(kPatThreads) pattern_kernel(
     const float* __restrict__ a_hat, int H, int G, int n, int nb, int b, float scale, float tau,
     float* __restrict__ a_bar, int32_t* __restrict__ pattern_ws, float* __restrict__ jsd_ws,
     int32_t* __restrict__ pattern_out, float* __restrict__ jsd_out) {
+  FP_PDL_ENTRY();
   extern __shared__ __align__(16) float psm[];  // qbar[128] | qpart[4][128] | logits[nb] | red[33]
   float* qbar = psm;
   float* qpart = psm + 128;
@@ -216,6 +220,7 @@ __global__ void __launch_bounds__(kPatThreads) pattern_kernel(
 __global__ void __launch_bounds__(256) qbar_kernel(const __nv_bfloat16* __restrict__ q, TLayout ql,
                                                    const int32_t* __restrict__ pattern, int n, int nb,
                                                    int b, float* __restrict__ q_bar) {
+  FP_PDL_ENTRY();
   __shared__ float red[16][128];
   const int qb = blockIdx.x, h = blockIdx.y;
   if (pattern && pattern[h] != 1) return;  // pattern == nullptr: every head
@@ -260,6 +265,7 @@ __global__ void __launch_bounds__(64) pooled_logits(
     const float* __restrict__ q_bar, const float* __restrict__ k_bar,
     const int32_t* __restrict__ pattern, int H, int G, int nb, float scale,
     float* __restrict__ A_bar) {
+  FP_PDL_ENTRY();
   const int h = blockIdx.y;
   if (pattern && pattern[h] != 1) return;
   // triangular decode of blockIdx.x = rt (rt + 1) / 2 + ct
@@ -317,6 +323,7 @@ __global__ void __launch_bounds__(64) pooled_logits(
 constexpr int kMapThreads = 256;
 __global__ void __launch_bounds__(kMapThreads) pooled_softmax(const int32_t* __restrict__ pattern,
                                                               int nb, float* __restrict__ A_bar) {
+  FP_PDL_ENTRY();
   __shared__ float red[33];
   const int qb = blockIdx.x, h = blockIdx.y;
   if (pattern && pattern[h] != 1) return;
@@ -399,20 +406,20 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
   cudaStream_t sq = side ? side : st;
   const int nt = (s.nb + kPT - 1) / kPT;
   if (side)  // q_bar does not need K_bar: start it at the fork
-    qbar_kernel<<<dim3(s.nb, s.H), 256, 0, sq>>>(reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
+    FP_LAUNCH(qbar_kernel, dim3(s.nb, s.H), 256, 0, sq, reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
                                                  qa_only, s.n, s.nb, s.b, wsp<float>(ws, L.q_bar));
   auto pooled_map = [&]() {
     if (!side)
-      qbar_kernel<<<dim3(s.nb, s.H), 256, 0, sq>>>(reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
+      FP_LAUNCH(qbar_kernel, dim3(s.nb, s.H), 256, 0, sq, reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
                                                    qa_only, s.n, s.nb, s.b, wsp<float>(ws, L.q_bar));
     if (side) chk(cudaStreamWaitEvent(side, e_kbar, 0));  // K_bar from the second pass
-    pooled_logits<<<dim3(nt * (nt + 1) / 2, s.H), 64, 0, sq>>>(wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar),
+    FP_LAUNCH(pooled_logits, dim3(nt * (nt + 1) / 2, s.H), 64, 0, sq, wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar),
                                                      qa_only, s.H, s.G, s.nb, scale,
                                                      wsp<float>(ws, L.A_bar));
-    pooled_softmax<<<dim3(s.nb, s.H), kMapThreads, 0, sq>>>(qa_only, s.nb, wsp<float>(ws, L.A_bar));
+    FP_LAUNCH(pooled_softmax, dim3(s.nb, s.H), kMapThreads, 0, sq, qa_only, s.nb, wsp<float>(ws, L.A_bar));
   };
   chk(launch_rep(s, qmap, kmap, Hp, Gp, scale_log2, m_part, l_part, nullptr, nullptr, nullptr, nullptr, 1, st));
-  rep_stats<<<s.H, 128, 0, st>>>(s.nchunks, 128 - s.b, m_part, l_part, m_row, mp_row);
+  FP_LAUNCH(rep_stats, s.H, 128, 0, st, s.nchunks, 128 - s.b, m_part, l_part, m_row, mp_row);
   chk(launch_rep(s, qmap, kmap, Hp, Gp, scale_log2, nullptr, nullptr, mp_row, wsp<float>(ws, L.k_bar),
                  wsp<float>(ws, L.a_v), wsp<float>(ws, L.as_part), 2, st));
   if (side) {
@@ -420,14 +427,14 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
     pooled_map();
     chk(cudaEventRecord(e_join, side));
   }
-  slash_combine<<<dim3((s.n + 255) / 256, s.H), 256, 0, st>>>(s.n, s.nt, 1.0f / (float)s.b,
+  FP_LAUNCH(slash_combine, dim3((s.n + 255) / 256, s.H), 256, 0, st, s.n, s.nt, 1.0f / (float)s.b,
                                                               wsp<float>(ws, L.as_part),
                                                               wsp<float>(ws, L.a_s));
-  block_sums<<<dim3(s.nb, s.H), 128, 0, st>>>(s.n, s.nb, s.b, wsp<float>(ws, L.a_v),
+  FP_LAUNCH(block_sums, dim3(s.nb, s.H), 128, 0, st, s.n, s.nb, s.b, wsp<float>(ws, L.a_v),
                                               wsp<float>(ws, L.a_s), wsp<float>(ws, L.a_hat),
                                               wsp<float>(ws, L.As));
   const size_t psm = (128 + 512 + (size_t)s.nb + 33) * 4;
-  pattern_kernel<<<s.H, kPatThreads, psm, st>>>(
+  FP_LAUNCH(pattern_kernel, s.H, kPatThreads, psm, st, 
       reinterpret_cast<const __nv_bfloat16*>(q), lay.q, wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_hat),
       s.H, s.G, s.n, s.nb, s.b, scale, tau, wsp<float>(ws, L.a_bar), wsp<int32_t>(ws, L.pattern),
       wsp<float>(ws, L.jsd), pattern_out, jsd_out);

@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
                    int32_t* __restrict__ sel_v, int32_t* __restrict__ sel_s,
                    int32_t* __restrict__ sel_qa, int32_t* __restrict__ sel_count,
                    unsigned long long* __restrict__ sel_mass) {
+  FP_PDL_ENTRY();
   extern __shared__ __align__(16) uint8_t top_raw[];
   TopSmem& sm = *reinterpret_cast<TopSmem*>(top_raw);
   uint32_t ncl;
@@ -448,6 +449,7 @@ __global__ void __launch_bounds__(kRowThreads) topmass_rows(
     const float* __restrict__ A_bar, const int32_t* __restrict__ pattern, int nb, int nbw,
     long long tri, float gamma, uint32_t* __restrict__ selbits, int32_t* __restrict__ sel_count,
     unsigned long long* __restrict__ sel_mass) {
+  FP_PDL_ENTRY();
   __shared__ RowSmem sm;
   const int qb = blockIdx.x, h = blockIdx.y;
   if (pattern[h] != 1) return;
@@ -570,6 +572,7 @@ __global__ void build_lines(const int32_t* __restrict__ pattern, const int32_t* 
                             const int32_t* __restrict__ sel_s, const int32_t* __restrict__ sel_count,
                             int n, int nb, int nbw, int vs_mode, int lb, uint32_t* __restrict__ vbits,
                             uint32_t* __restrict__ dbits) {
+  FP_PDL_ENTRY();
   extern __shared__ uint32_t bsm[];  // V[nbw] | D[nbw]
   const int h = blockIdx.x;
   uint32_t* V = bsm;
@@ -613,6 +616,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows(
     int max_blocks, uint32_t* __restrict__ rowbits, int32_t* __restrict__ row_nnz,
     int32_t* __restrict__ row_nnz_pre, int32_t* __restrict__ budget_added,
     int32_t* __restrict__ budget_removed) {
+  FP_PDL_ENTRY();
   extern __shared__ uint32_t asmem[];  // [kAsmWarps][2][nbw]
   const int h = blockIdx.y;
   const int w = warp_id(), ln = lane_id();
@@ -749,6 +753,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
              const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_count,
              const unsigned long long* __restrict__ sel_mass, int nb, int32_t* __restrict__ row_ptr,
              fp_select_stats* __restrict__ stats) {
+  FP_PDL_ENTRY();
   __shared__ uint64_t wsum[32];
   const int h = blockIdx.x;
   uint64_t run = 0, badd = 0, brem = 0;
@@ -789,6 +794,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
 __global__ void __launch_bounds__(kAsmWarps * 32) write_cols(
     const uint32_t* __restrict__ rowbits, const int32_t* __restrict__ row_ptr, int nb, int nbw,
     long long cap, int32_t* __restrict__ col_idx) {
+  FP_PDL_ENTRY();
   const int h = blockIdx.y;
   const int w = warp_id(), ln = lane_id();
   const int qb = blockIdx.x * kAsmWarps + w;
@@ -824,13 +830,19 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
     cfg.blockDim = dim3(kSelThreads);
     cfg.dynamicSmemBytes = sizeof(TopSmem);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = ncl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (FP_PDL_ENTRY)
+#ifdef FP_NO_PDL
+    attr[1].val.programmaticStreamSerializationAllowed = 0;
+#else
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+#endif
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(
         &cfg, topmass_kernel, (const float*)wsp<float>(ws, L.a_v), (const float*)wsp<float>(ws, L.a_s),
         (const float*)wsp<float>(ws, L.a_hat), (const float*)wsp<float>(ws, L.As),
@@ -841,10 +853,10 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
     if (e != cudaSuccess) return e;
   }
   if (opt.qa_mode == 1)
-    topmass_rows<<<dim3(s.nb, s.H), kRowThreads, 0, st>>>(
+    FP_LAUNCH(topmass_rows, dim3(s.nb, s.H), kRowThreads, 0, st, 
         wsp<float>(ws, L.A_bar), pat, s.nb, L.nbw, s.tri, gamma, wsp<uint32_t>(ws, L.selbits),
         wsp<int32_t>(ws, L.sel_count), wsp<unsigned long long>(ws, L.sel_mass));
-  build_lines<<<s.H, 1024, 2 * L.nbw * 4, st>>>(pat, wsp<int32_t>(ws, L.sel_v),
+  FP_LAUNCH(build_lines, s.H, 1024, 2 * L.nbw * 4, st, pat, wsp<int32_t>(ws, L.sel_v),
                                                 wsp<int32_t>(ws, L.sel_s),
                                                 wsp<int32_t>(ws, L.sel_count), s.n, s.nb, L.nbw,
                                                 opt.vs_mode, s.lb, wsp<uint32_t>(ws, L.vbits),
@@ -854,18 +866,18 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
   const int min_blocks = (int)std::min<long long>(s.nb, ((long long)min_budget + s.b - 1) / s.b);
   const int max_blocks = (int)std::min<long long>(s.nb, ((long long)opt.max_budget + s.b - 1) / s.b);
   const dim3 rg((s.nb + kAsmWarps - 1) / kAsmWarps, s.H);
-  assemble_rows<<<rg, kAsmWarps * 32, kAsmWarps * 2 * L.nbw * 4, st>>>(
+  FP_LAUNCH(assemble_rows, rg, kAsmWarps * 32, kAsmWarps * 2 * L.nbw * 4, st, 
       pat, wsp<uint32_t>(ws, L.vbits), wsp<uint32_t>(ws, L.dbits), wsp<int32_t>(ws, L.sel_qa),
       wsp<int32_t>(ws, L.sel_count), wsp<float>(ws, L.a_hat), wsp<float>(ws, L.As),
       wsp<float>(ws, L.A_bar), s.nb, L.nbw, s.tri, min_blocks, opt.qa_mode,
       wsp<uint32_t>(ws, L.selbits), max_blocks, wsp<uint32_t>(ws, L.rowbits),
       wsp<int32_t>(ws, L.row_nnz), wsp<int32_t>(ws, L.row_nnz_pre), wsp<int32_t>(ws, L.budget_added),
       wsp<int32_t>(ws, L.budget_removed));
-  row_scan<<<s.H, kSelThreads, 0, st>>>(wsp<int32_t>(ws, L.row_nnz), wsp<int32_t>(ws, L.budget_added),
+  FP_LAUNCH(row_scan, s.H, kSelThreads, 0, st, wsp<int32_t>(ws, L.row_nnz), wsp<int32_t>(ws, L.budget_added),
                                         wsp<int32_t>(ws, L.budget_removed), pat,
                                         wsp<int32_t>(ws, L.sel_count),
                                         wsp<unsigned long long>(ws, L.sel_mass), s.nb, row_ptr, stats);
-  write_cols<<<rg, kAsmWarps * 32, 0, st>>>(wsp<uint32_t>(ws, L.rowbits), row_ptr, s.nb, L.nbw,
+  FP_LAUNCH(write_cols, rg, kAsmWarps * 32, 0, st, wsp<uint32_t>(ws, L.rowbits), row_ptr, s.nb, L.nbw,
                                             s.tri, col_idx);
   return cudaGetLastError();
 }
