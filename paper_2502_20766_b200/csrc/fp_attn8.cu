@@ -46,9 +46,12 @@
 #ifdef FP_TIMING
 // clock64 phase accumulators (tools/attn8_timing.py): [0..5] softmax thread 0
 // of each row, [8..12] the MMA issuer, [14] issuer entries, [15] softmax tiles
-__device__ unsigned long long g_attn8_timing[16];
+__device__ unsigned long long g_attn8_timing[20];
+// [16] p_full arrival (thread 0 of the row) -> the issuer's wait returns,
+// [17] S commit issued -> the row's softmax wait returns, [18] count of [16], [19] count of [17]
+__device__ long long g_attn8_ts[148 * 4];
 #define FP_T8(k) do { if (t_on) { long long _t = clock64(); tacc[k] += _t - tlast; tlast = _t; } } while (0)
-#define FP_T8_DECL(on) const bool t_on = (on); long long tacc[16] = {0}; long long tlast = clock64()
+#define FP_T8_DECL(on) const bool t_on = (on); long long tacc[20] = {0}; long long tlast = clock64()
 #define FP_T8_FLUSH(lo, hi) do { if (t_on) for (int _k = lo; _k < hi; ++_k) atomicAdd(&g_attn8_timing[_k], (unsigned long long)tacc[_k]); } while (0)
 #else
 #define FP_T8(k) do { } while (0)
@@ -277,17 +280,26 @@ struct Item {
   const int32_t* lb;
 };
 template <bool DENSE>
+// order_gm = 0 (all K/V fit comfortably in L2, short n): pair-major over all
+// heads, so every group's costliest pairs start in the first wave (a
+// group-major order leaves the last groups' long rows as a tail).
 FP_DEV Item decode_item(int item, int H, int G, int nb, long long cap, const int32_t* row_ptr,
-                        const int32_t* col_idx) {
+                        const int32_t* col_idx, int order_gm) {
   Item it;
   const int gsz = H / G;
   const int npair = (nb + 1) >> 1;
-  const int per_group = gsz * npair;
-  it.g = item / per_group;
-  const int rem = item - it.g * per_group;
-  it.qbA = nb - 1 - 2 * (rem / gsz);
+  if (order_gm) {
+    const int per_group = gsz * npair;
+    it.g = item / per_group;
+    const int rem = item - it.g * per_group;
+    it.qbA = nb - 1 - 2 * (rem / gsz);
+    it.h = it.g * gsz + rem % gsz;
+  } else {
+    it.qbA = nb - 1 - 2 * (item / H);
+    it.h = item % H;
+    it.g = it.h / gsz;
+  }
   it.qbB = it.qbA - 1;  // -1: no row B
-  it.h = it.g * gsz + rem % gsz;
   it.la = it.lb = nullptr;
   if (DENSE) {
     it.nA = it.qbA + 1;
@@ -334,7 +346,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
                  const TLayout ol, int Hp, int Gp, int H, int G, int n, int nb, long long cap,
                  const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                  float scale_log2, const unsigned long long* __restrict__ peer_o, int n_peer,
-                 int total_items, int* __restrict__ sched) {
+                 int total_items, int* __restrict__ sched, int order_gm) {
   FP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 tiles need 1024-B alignment
@@ -447,7 +459,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
             mbar_arrive(&sm.item_empty[k & 1]);
           }
           if (item < 0) break;
-          const Item it = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx);
+          const Item it = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx, order_gm);
           if (isK) {
             // Q_A, Q_B of this item once the previous item's S MMAs are done
             if (k >= 1) mbar_wait(&sm.q_empty, (k - 1) & 1);
@@ -492,7 +504,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
           __syncwarp();
           if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
           if (item < 0) break;
-          const Item itm = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx);
+          const Item itm = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx, order_gm);
           int pend[2] = {-1, -1};  // union entry of X's S awaiting its PV
           int lcnt[2] = {0, 0};    // S tiles issued per stream in this item
           auto issue_pv = [&](int x) {
@@ -510,6 +522,11 @@ __global__ void __launch_bounds__(kThreads8, 1)
               FP_T8(12);
               mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
               FP_T8(11);
+#ifdef FP_TIMING
+              if (t_on) {
+                tacc[16] += clock64() - *(volatile long long*)&g_attn8_ts[blockIdx.x * 4 + x];
+              }
+#endif
               tc_fence_after();
               PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512, idesc_o, 1);
             } else {
@@ -547,6 +564,9 @@ __global__ void __launch_bounds__(kThreads8, 1)
 #endif
                 FP_T8(13);  // issue time of the 8 S MMAs
                 COMMIT8(&sm.s_full[x]);
+#ifdef FP_TIMING
+                if (t_on) *(volatile long long*)&g_attn8_ts[blockIdx.x * 4 + 2 + x] = clock64();
+#endif
                 pend[x] = e;
                 ++cnt[x];
                 ++lcnt[x];
@@ -564,6 +584,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
         }
         FP_T8(12);
         FP_T8_FLUSH(8, 15);
+        FP_T8_FLUSH(16, 17);
       }
     }
   } else {
@@ -581,7 +602,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
       if (item < 0) break;
-      const Item itm = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx);
+      const Item itm = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx, order_gm);
       const bool exact = (item & kExact8) != 0;
       const int nX = x ? itm.nB : itm.nA;
       const int qb = x ? itm.qbB : itm.qbA;
@@ -591,6 +612,9 @@ __global__ void __launch_bounds__(kThreads8, 1)
         FP_T8(6);
         mbar_wait(&sm.s_full[x], ph);
         FP_T8(0);
+#ifdef FP_TIMING
+        if (t_on && t > 0) tacc[17] += clock64() - *(volatile long long*)&g_attn8_ts[blockIdx.x * 4 + 2 + x];
+#endif
 #ifdef FP_XSM8
         // experiment: softmax does no work (measures the MMA/issuer pipeline alone)
         tc_fence_after();
@@ -692,6 +716,9 @@ __global__ void __launch_bounds__(kThreads8, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
+#ifdef FP_TIMING
+        if (t_on) *(volatile long long*)&g_attn8_ts[blockIdx.x * 4 + x] = clock64();
+#endif
         if (lane_id() == 0) mbar_arrive(&sm.p_full[x]);
         // the row sum after P is handed over (off the PV's critical path)
         l = fmaf(l, alpha, (s0 + s1) + (s2 + s3));
@@ -750,6 +777,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
       }
     }
     FP_T8_FLUSH(0, 8);
+    FP_T8_FLUSH(17, 18);
 #ifdef FP_TIMING
     if (t_on) atomicAdd(&g_attn8_timing[15], (unsigned long long)tacc[15]);
 #endif
@@ -765,9 +793,9 @@ size_t attn8_smem_bytes() { return sizeof(Attn8Smem); }
 
 #ifdef FP_TIMING
 extern "C" int fp_debug_attn8_timing(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, g_attn8_timing, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out, g_attn8_timing, sizeof(unsigned long long) * 20);
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[20] = {0};
     cudaMemcpyToSymbol(g_attn8_timing, z, sizeof(z));
   }
   return 0;
@@ -786,6 +814,9 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const float scale_log2 = (1.0f / sqrtf(128.0f)) * kLog2e;
   const int total = s.H * ((s.nb + 1) / 2);
+  // KV-group-major item order when the layer's K/V exceed half the L2 (one
+  // group's K/V then stays resident while its items run), pair-major otherwise
+  const int order_gm = (double)s.G * s.n * 128 * 2 * 2 > 64.0 * 1024 * 1024 ? 1 : 0;
   // persistent (one CTA per SM, dynamic work fetch) when a workspace holds the
   // scheduler; otherwise one CTA per item (a static round-robin over a
   // persistent grid would leave the per-item cost variance unbalanced)
@@ -799,11 +830,11 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
   if (dense)
     FP_LAUNCH(attn8_kernel<true>, grid, kThreads8, smem, st, qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per, s.H,
                                                       s.G, s.n, s.nb, s.tri, row_ptr, col_idx, scale_log2,
-                                                      po, n_peer, total, sched);
+                                                      po, n_peer, total, sched, order_gm);
   else
     FP_LAUNCH(attn8_kernel<false>, grid, kThreads8, smem, st, qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per,
                                                        s.H, s.G, s.n, s.nb, s.tri, row_ptr, col_idx,
-                                                       scale_log2, po, n_peer, total, sched);
+                                                       scale_log2, po, n_peer, total, sched, order_gm);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,10 @@
 namespace fp {
 
 constexpr int kChunkTilesMax = 8;  // key tiles (128 keys) per representative-pass CTA (max)
+#ifndef FP_MIN_CHUNKS
+#define FP_MIN_CHUNKS 16
+#endif
+constexpr int kMinChunks = FP_MIN_CHUNKS;  // representative-pass chunks per head (min, see make_shape)
 
 struct Shape {
   int H, G, n, nb, nchunks, g;  // flattened heads (batch * heads per sequence); g = H / G
@@ -29,15 +33,17 @@ inline Shape make_shape(int heads, int kv_heads, int seq_len, int block = 128) {
   s.lb = block == 64 ? 6 : 7;
   s.nb = (seq_len + block - 1) / block;  // ragged n: the last block is partial (A26)
   s.nt = (seq_len + 127) / 128;
-  // key tiles per representative-pass CTA: the largest chunk (<= 8 tiles) that
-  // leaves >= 32 chunks per head. A function of n ONLY: pass 1 sums each row's
+  // key tiles per representative-pass CTA: the largest power of two <= 8 that
+  // leaves >= 8 chunks per head (short sequences: a few CTAs with several
+  // tiles each instead of many one-tile CTAs whose setup dominates; measured
+  // at 4k). A function of n ONLY: pass 1 sums each row's
   // exponentials within a chunk and rep_stats combines the chunks, so the fp32
   // summation order of the row statistics (and of everything derived from them:
   // a_v, a_s, a_hat, D_JS, the top-mass picks) must not depend on how many
   // heads one call batches (fp_layer_host per-group calls, multi-GPU head
   // slices and the whole-layer call give bitwise identical results).
   s.ct = kChunkTilesMax;
-  while (s.ct > 1 && (s.nt + s.ct - 1) / s.ct < 32) s.ct >>= 1;
+  while (s.ct > 1 && (s.nt + s.ct - 1) / s.ct < kMinChunks) s.ct >>= 1;
   s.nchunks = (s.nt + s.ct - 1) / s.ct;
   s.g = heads / kv_heads;
   s.tri = (long long)s.nb * (s.nb + 1) / 2;

@@ -37,7 +37,14 @@ for p in a.libs:
     L = ctypes.CDLL(os.path.abspath(p), mode=os.RTLD_LOCAL)
     L.fp_plan.argtypes = [P, P, I, I, I, I, I, F, P, Z, P, P, P]
     L.fp_select.argtypes = [I, I, I, I, I, F, I, P, Z, P, P, P, P]
+    L.fp_workspace_bytes.restype = Z
+    L.fp_workspace_bytes.argtypes = [I, I, I, I, I]
     libs.append(L)
+# one workspace large enough for every build's layout
+wsb = max(L.fp_workspace_bytes(w.heads, w.kv_heads, w.seq_len, 128, 128) for L in libs)
+if wsb > fpl.ws_bytes:
+    fpl.ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")
+    fpl.ws_bytes = wsb
 st = torch.cuda.current_stream().cuda_stream
 
 
