@@ -36,7 +36,7 @@ fpl.plan(q, k, w.tau)
 fpl.select(w.gamma, w.min_budget)
 run = (lambda: fpl.dense(q, k, v, out)) if a.dense else (lambda: fpl.attn(q, k, v, out))
 raw = ctypes.CDLL(os.path.abspath(a.lib))
-buf = (ctypes.c_ulonglong * 16)()
+buf = (ctypes.c_ulonglong * 20)()
 dbg = raw.fp_debug_attn8_timing
 run()
 torch.cuda.synchronize()
@@ -61,3 +61,7 @@ itot = sum(buf[i] for i in inames)
 for i, nm in inames.items():
     print(f"  issuer  {nm:16s} {buf[i] / ents:8.1f} cyc/entry  {100 * buf[i] / max(itot, 1):5.1f}%")
 print(f"  issuer total             {itot / ents:8.1f} cyc/entry")
+
+if not a.v11:
+    print(f"  handoff p_full -> issuer wake   {buf[16] / ents:8.1f} cyc/entry (row A + B, thread 0's arrival)")
+    print(f"  S commit -> softmax wake        {buf[17] / tiles:8.1f} cyc/tile (incl. the S MMAs still executing)")
