@@ -218,12 +218,17 @@ __global__ void __launch_bounds__(kPatThreads) pattern_kernel(
 // (block, head): thread t sums 8 dims (one 16-B load per row) of b/16 rows,
 // the 16 row groups are combined in a fixed order.
 __global__ void __launch_bounds__(256) qbar_kernel(const __nv_bfloat16* __restrict__ q, TLayout ql,
-                                                   const int32_t* __restrict__ pattern, int n, int nb,
-                                                   int b, float* __restrict__ q_bar) {
+                                                   const int32_t* __restrict__ pattern, int H, int n,
+                                                   int nb, int b, float* __restrict__ q_bar) {
   FP_PDL_ENTRY();
   __shared__ float red[16][128];
-  const int qb = blockIdx.x, h = blockIdx.y;
-  if (pattern && pattern[h] != 1) return;  // pattern == nullptr: every head
+  const int qb = blockIdx.x;
+  // heads [h_lo, h_hi) of this CTA (one each when every head is pooled; the
+  // Query-Aware heads of a range otherwise: no CTA per skipped head)
+  const int h_lo = blockIdx.y * H / gridDim.y, h_hi = (blockIdx.y + 1) * H / gridDim.y;
+  for (int h = h_lo; h < h_hi; ++h) {
+  if (pattern && pattern[h] != 1) continue;  // pattern == nullptr: every head
+  __syncthreads();  // red[] of the previous head consumed
   const int tid = threadIdx.x;
   const int c8 = tid & 15, rg = tid >> 4, rows = b >> 4;
   const int cnt = min(b, n - qb * b);
@@ -251,6 +256,7 @@ __global__ void __launch_bounds__(256) qbar_kernel(const __nv_bfloat16* __restri
     for (int g2 = 0; g2 < 16; ++g2) sum += red[g2][tid];
     q_bar[((size_t)h * nb + qb) * 128 + tid] = sum / (float)cnt;
   }
+  }
 }
 
 // A_bar[qb, kb <= qb] = softmax_row(scale * Qbar[qb] . Kbar[kb]) / nb  (A5)
@@ -266,8 +272,7 @@ __global__ void __launch_bounds__(64) pooled_logits(
     const int32_t* __restrict__ pattern, int H, int G, int nb, float scale,
     float* __restrict__ A_bar) {
   FP_PDL_ENTRY();
-  const int h = blockIdx.y;
-  if (pattern && pattern[h] != 1) return;
+  const int h_lo = blockIdx.y * H / gridDim.y, h_hi = (blockIdx.y + 1) * H / gridDim.y;
   // triangular decode of blockIdx.x = rt (rt + 1) / 2 + ct
   int rt = (int)((sqrtf(8.0f * (float)blockIdx.x + 1.0f) - 1.0f) * 0.5f);
   while ((rt + 1) * (rt + 2) / 2 <= (int)blockIdx.x) ++rt;
@@ -277,8 +282,11 @@ __global__ void __launch_bounds__(64) pooled_logits(
   // consecutive float4s per warp instruction (conflict-free shared loads)
   __shared__ float4 qs4[32][kPT];
   __shared__ float4 ks4[32][kPT];
-  const int g = h / (H / G);
   const int tid = threadIdx.x;
+  for (int h = h_lo; h < h_hi; ++h) {
+  if (pattern && pattern[h] != 1) continue;
+  __syncthreads();  // the previous head's tiles are consumed
+  const int g = h / (H / G);
   for (int e = tid; e < kPT * 32; e += 64) {
     const int rr = e >> 5, d4 = e & 31;
     const int qb = rt * kPT + rr, kb = ct * kPT + rr;
@@ -318,15 +326,18 @@ __global__ void __launch_bounds__(64) pooled_logits(
       if (kb <= qb) row[kb] = acc[i][j] * scale;
     }
   }
+  }
 }
 
 constexpr int kMapThreads = 256;
 __global__ void __launch_bounds__(kMapThreads) pooled_softmax(const int32_t* __restrict__ pattern,
-                                                              int nb, float* __restrict__ A_bar) {
+                                                              int H, int nb, float* __restrict__ A_bar) {
   FP_PDL_ENTRY();
   __shared__ float red[33];
-  const int qb = blockIdx.x, h = blockIdx.y;
-  if (pattern && pattern[h] != 1) return;
+  const int qb = blockIdx.x;
+  const int h_lo = blockIdx.y * H / gridDim.y, h_hi = (blockIdx.y + 1) * H / gridDim.y;
+  for (int h = h_lo; h < h_hi; ++h) {
+  if (pattern && pattern[h] != 1) continue;
   float* row = A_bar + (size_t)h * ((size_t)nb * (nb + 1) / 2) + (size_t)qb * (qb + 1) / 2;
   const int tid = threadIdx.x;
   float mx = -INFINITY;
@@ -337,6 +348,7 @@ __global__ void __launch_bounds__(kMapThreads) pooled_softmax(const int32_t* __r
   se = block_sum<kMapThreads>(se, red);
   const float inv_nb = 1.0f / (float)nb;
   for (int kb = tid; kb <= qb; kb += kMapThreads) row[kb] = (expf(row[kb] - mx) / se) * inv_nb;
+  }
 }
 
 }  // namespace
@@ -405,18 +417,21 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
   const int32_t* qa_only = side ? nullptr : wsp<int32_t>(ws, L.pattern);
   cudaStream_t sq = side ? side : st;
   const int nt = (s.nb + kPT - 1) / kPT;
+  // one CTA per head when every head is pooled (short n, side stream);
+  // otherwise CTAs over head ranges that skip the Vertical-Slash heads
+  const int hy = qa_only ? std::min(s.H, 4) : s.H;
   if (side)  // q_bar does not need K_bar: start it at the fork
-    FP_LAUNCH(qbar_kernel, dim3(s.nb, s.H), 256, 0, sq, reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
-                                                 qa_only, s.n, s.nb, s.b, wsp<float>(ws, L.q_bar));
+    FP_LAUNCH(qbar_kernel, dim3(s.nb, hy), 256, 0, sq, reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
+                                                 qa_only, s.H, s.n, s.nb, s.b, wsp<float>(ws, L.q_bar));
   auto pooled_map = [&]() {
     if (!side)
-      FP_LAUNCH(qbar_kernel, dim3(s.nb, s.H), 256, 0, sq, reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
-                                                   qa_only, s.n, s.nb, s.b, wsp<float>(ws, L.q_bar));
+      FP_LAUNCH(qbar_kernel, dim3(s.nb, hy), 256, 0, sq, reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
+                                                   qa_only, s.H, s.n, s.nb, s.b, wsp<float>(ws, L.q_bar));
     if (side) chk(cudaStreamWaitEvent(side, e_kbar, 0));  // K_bar from the second pass
-    FP_LAUNCH(pooled_logits, dim3(nt * (nt + 1) / 2, s.H), 64, 0, sq, wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar),
+    FP_LAUNCH(pooled_logits, dim3(nt * (nt + 1) / 2, hy), 64, 0, sq, wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar),
                                                      qa_only, s.H, s.G, s.nb, scale,
                                                      wsp<float>(ws, L.A_bar));
-    FP_LAUNCH(pooled_softmax, dim3(s.nb, s.H), kMapThreads, 0, sq, qa_only, s.nb, wsp<float>(ws, L.A_bar));
+    FP_LAUNCH(pooled_softmax, dim3(s.nb, hy), kMapThreads, 0, sq, qa_only, s.H, s.nb, wsp<float>(ws, L.A_bar));
   };
   chk(launch_rep(s, qmap, kmap, Hp, Gp, scale_log2, m_part, l_part, nullptr, nullptr, nullptr, nullptr, 1, st));
   FP_LAUNCH(rep_stats, s.H, 128, 0, st, s.nchunks, 128 - s.b, m_part, l_part, m_row, mp_row);
