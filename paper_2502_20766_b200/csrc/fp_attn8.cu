@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
                 FP_T8(12);
 #if !defined(FP_XMMA8) && !defined(FP_XS8)
                 SSCHAIN8(tbase + kColS8 + x * 128, qdesc[x], kdesc, idesc_s);
-#endif
+
                 FP_T8(13);  // issue time of the 8 S MMAs
                 COMMIT8(&sm.s_full[x]);
 #ifdef FP_TIMING
@@ -572,6 +572,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
                 ++lcnt[x];
               }
             }
+#endif
             COMMIT8(&sm.k_empty[ks]);
             // an entry only one row uses gets its second V-slot release here
             // (it arrives early, but the phase also needs the PV's commit)

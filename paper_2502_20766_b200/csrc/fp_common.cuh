@@ -72,6 +72,18 @@ FP_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Non-blocking test of phase completion (for polling several barriers).
+FP_DEV bool mbar_test(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // Wait for the phase with parity `parity` to complete. A wait that exceeds
 // ~2^34 cycles (seconds) is a pipeline bug: trap instead of hanging the GPU.
 FP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
