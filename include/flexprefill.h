@@ -232,9 +232,8 @@ fp_status fp_sparse_attn_ex(const void* q, const void* k, const void* v, void* o
  * the kernel (e.g. the symmetric-memory barrier on the same stream) before a
  * peer reads its buffer. Errors: FP_ERR_RANGE n_peer < 0 or > FP_MAX_PEERS;
  * FP_ERR_NULL peer_o NULL with n_peer > 0; FP_ERR_ALIGN peer_o not 8-B
- * aligned (the pointer values are device data and are not checked). Only the
- * default attention kernel (v8) at block_size 128 implements it; otherwise the
- * call fails with FP_ERR_CUDA (cudaErrorNotSupported). */
+ * aligned (the pointer values are device data and are not checked). Both
+ * block sizes (64 runs the same kernel on coarse 128 x 128 tiles). */
 #define FP_MAX_PEERS 8
 fp_status fp_sparse_attn_peers(const void* q, const void* k, const void* v, void* o,
                                const void* const* peer_o, int n_peer, int heads, int kv_heads,

@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libflexprefill.so")
-SOURCES = ["fp_api.cu", "fp_plan.cu", "fp_rep.cu", "fp_select.cu", "fp_attn.cu", "fp_attn8.cu", "fp_attn64.cu"]
+SOURCES = ["fp_api.cu", "fp_plan.cu", "fp_rep.cu", "fp_select.cu", "fp_attn.cu", "fp_attn8.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [

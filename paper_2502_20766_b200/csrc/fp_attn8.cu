@@ -39,6 +39,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "fp_common.cuh"
 #include "fp_internal.h"
@@ -271,20 +272,90 @@ struct UnionIter {
   }
 };
 
+// Block size 64 (reading A27): the attention runs on COARSE 128 x
+// 128 tiles. Coarse row J holds the 64-row query blocks 2J and 2J+1 (one
+// contiguous 128-row Q tile); its entries are the coarse key tiles m = kb / 2
+// of the union of the two 64-rows' sorted lists, each with a 4-bit mask, bit
+// 2 hx + hy = "query block 2J + hx selected key block 2m + hy". The softmax
+// sets every unselected 64 x 64 quadrant of its rows to -inf, so exactly the
+// selected blocks contribute; quadrants computed but masked are the price of
+// the 128-wide tensor-core tile. The two 64-rows of a coarse row are adjacent
+// in the 64-block CSR (row 2J+1 follows row 2J).
+struct CoarseRow {
+  const int32_t* l;  // row 2J's list; row 2J+1's follows it
+  int n0, n1, i0, i1;
+  FP_DEV void init(const int32_t* l_, int n0_, int n1_) {
+    l = l_;
+    n0 = n0_;
+    n1 = n1_;
+    i0 = i1 = 0;
+  }
+  FP_DEV bool done() const { return i0 >= n0 && i1 >= n1; }
+  FP_DEV int peek() const {
+    const int a = i0 < n0 ? (__ldg(l + i0) >> 1) : 0x7fffffff;
+    const int b = i1 < n1 ? (__ldg(l + n0 + i1) >> 1) : 0x7fffffff;
+    return min(a, b);
+  }
+  FP_DEV int next(int& mask) {  // coarse key tile m, quadrant mask
+    const int m = peek();
+    mask = 0;
+    while (i0 < n0) {
+      const int x = __ldg(l + i0);
+      if ((x >> 1) != m) break;
+      mask |= 1 << (x & 1);
+      ++i0;
+    }
+    while (i1 < n1) {
+      const int x = __ldg(l + n0 + i1);
+      if ((x >> 1) != m) break;
+      mask |= 4 << (x & 1);
+      ++i1;
+    }
+    return m;
+  }
+};
+// Union of the coarse rows A and B (mask bit 0: A has the tile, bit 1: B).
+struct CoarseUnion {
+  CoarseRow a, b;
+  int ca, cb;
+  FP_DEV void init(const int32_t* la, int na0, int na1, const int32_t* lb, int nb0, int nb1) {
+    a.init(la, na0, na1);
+    b.init(lb, nb0, nb1);
+    ca = a.done() ? 0x7fffffff : a.peek();
+    cb = b.done() ? 0x7fffffff : b.peek();
+  }
+  FP_DEV bool done() const { return ca == 0x7fffffff && cb == 0x7fffffff; }
+  FP_DEV int next(int& mask) {
+    const int k = min(ca, cb);
+    mask = (ca == k ? 1 : 0) | (cb == k ? 2 : 0);
+    int qm;
+    if (mask & 1) {
+      a.next(qm);
+      ca = a.done() ? 0x7fffffff : a.peek();
+    }
+    if (mask & 2) {
+      b.next(qm);
+      cb = b.done() ? 0x7fffffff : b.peek();
+    }
+    return k;
+  }
+};
+
 // One work item = (head h, q-block pair (qbA, qbB = qbA - 1)); items are
 // numbered KV-group-major, pairs descending, heads of a group interleaved (the
 // K/V of one group, 64 MiB at 128k, stay in L2 while its items run).
 struct Item {
   int h, g, qbA, qbB, nA, nB;
+  int nA1, nB1;  // COARSE: lengths of the second 64-rows (nA, nB: the first)
   const int32_t* la;
   const int32_t* lb;
 };
-template <bool DENSE>
+template <bool DENSE, bool COARSE>
 // order_gm = 0 (all K/V fit comfortably in L2, short n): pair-major over all
 // heads, so every group's costliest pairs start in the first wave (a
 // group-major order leaves the last groups' long rows as a tail).
 FP_DEV Item decode_item(int item, int H, int G, int nb, long long cap, const int32_t* row_ptr,
-                        const int32_t* col_idx, int order_gm) {
+                        const int32_t* col_idx, int order_gm, int nb64) {
   Item it;
   const int gsz = H / G;
   const int npair = (nb + 1) >> 1;
@@ -301,7 +372,24 @@ FP_DEV Item decode_item(int item, int H, int G, int nb, long long cap, const int
   }
   it.qbB = it.qbA - 1;  // -1: no row B
   it.la = it.lb = nullptr;
-  if (DENSE) {
+  it.nA1 = it.nB1 = 0;
+  if (COARSE) {
+    // 64-block CSR (nb64 rows of 64 queries); coarse row J = 64-rows 2J, 2J+1
+    const int32_t* rp = row_ptr + (size_t)it.h * (nb64 + 1);
+    const int r0 = 2 * it.qbA;
+    const int a0 = __ldg(rp + r0), a1 = __ldg(rp + r0 + 1);
+    it.la = col_idx + (size_t)it.h * cap + a0;
+    it.nA = a1 - a0;
+    it.nA1 = r0 + 1 < nb64 ? __ldg(rp + r0 + 2) - a1 : 0;
+    if (it.qbB >= 0) {
+      const int b0 = __ldg(rp + r0 - 2), b1 = __ldg(rp + r0 - 1);
+      it.lb = col_idx + (size_t)it.h * cap + b0;
+      it.nB = b1 - b0;
+      it.nB1 = a0 - b1;
+    } else {
+      it.nB = 0;
+    }
+  } else if (DENSE) {
     it.nA = it.qbA + 1;
     it.nB = it.qbB + 1;
   } else {
@@ -339,14 +427,14 @@ FP_DEV Item decode_item(int item, int H, int G, int nb, long long cap, const int
 // are still redone. The redo overwrites the item's output rows. sched
 // (optional workspace scratch, zeroed before the launch): [0] work counter,
 // [1] number of redone items (diagnostics).
-template <bool DENSE>
+template <bool DENSE, bool COARSE>
 __global__ void __launch_bounds__(kThreads8, 1)
     attn8_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                  const __grid_constant__ CUtensorMap vmap, __nv_bfloat16* __restrict__ o,
                  const TLayout ol, int Hp, int Gp, int H, int G, int n, int nb, long long cap,
                  const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                  float scale_log2, const unsigned long long* __restrict__ peer_o, int n_peer,
-                 int total_items, int* __restrict__ sched, int order_gm) {
+                 int total_items, int* __restrict__ sched, int order_gm, int nb64) {
   FP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (smem_u32(smem_raw) & 1023u) __trap();  // SW128 tiles need 1024-B alignment
@@ -459,7 +547,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
             mbar_arrive(&sm.item_empty[k & 1]);
           }
           if (item < 0) break;
-          const Item it = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx, order_gm);
+          const Item it = decode_item<DENSE, COARSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx, order_gm, nb64);
           if (isK) {
             // Q_A, Q_B of this item once the previous item's S MMAs are done
             if (k >= 1) mbar_wait(&sm.q_empty, (k - 1) & 1);
@@ -467,8 +555,9 @@ __global__ void __launch_bounds__(kThreads8, 1)
             tma_tile(sm.q[0], &qmap, &sm.q_full, it.qbA * 128, it.h, Hp);
             if (it.nB > 0) tma_tile(sm.q[1], &qmap, &sm.q_full, it.qbB * 128, it.h, Hp);
           }
-          UnionIter un;
-          un.init(it.la, it.lb, it.nA, it.nB, DENSE);
+          typename std::conditional<COARSE, CoarseUnion, UnionIter>::type un;
+          if constexpr (COARSE) un.init(it.la, it.nA, it.nA1, it.lb, it.nB, it.nB1);
+          else un.init(it.la, it.lb, it.nA, it.nB, DENSE);
           for (; !un.done(); ++e) {
             int mask;
             const int kb = un.next(mask);
@@ -504,7 +593,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
           __syncwarp();
           if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
           if (item < 0) break;
-          const Item itm = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx, order_gm);
+          const Item itm = decode_item<DENSE, COARSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx, order_gm, nb64);
           int pend[2] = {-1, -1};  // union entry of X's S awaiting its PV
           int lcnt[2] = {0, 0};    // S tiles issued per stream in this item
           auto issue_pv = [&](int x) {
@@ -540,8 +629,9 @@ __global__ void __launch_bounds__(kThreads8, 1)
             pend[x] = -1;
           };
           mbar_wait(&sm.q_full, k & 1);
-          UnionIter un;
-          un.init(itm.la, itm.lb, itm.nA, itm.nB, DENSE);
+          typename std::conditional<COARSE, CoarseUnion, UnionIter>::type un;
+          if constexpr (COARSE) un.init(itm.la, itm.nA, itm.nA1, itm.lb, itm.nB, itm.nB1);
+          else un.init(itm.la, itm.lb, itm.nA, itm.nB, DENSE);
           for (; !un.done(); ++e) {
             int mask;
             un.next(mask);
@@ -603,12 +693,20 @@ __global__ void __launch_bounds__(kThreads8, 1)
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&sm.item_empty[k & 1]);
       if (item < 0) break;
-      const Item itm = decode_item<DENSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx, order_gm);
+      const Item itm = decode_item<DENSE, COARSE>(item & ~kExact8, H, G, nb, cap, row_ptr, col_idx, order_gm, nb64);
       const bool exact = (item & kExact8) != 0;
-      const int nX = x ? itm.nB : itm.nA;
+      // COARSE: this row's own coarse entries (for the quadrant masks); the
+      // tile count is only known when the walk ends
+      CoarseRow crow;
+      if (COARSE) crow.init(x ? itm.lb : itm.la, x ? itm.nB : itm.nA, x ? itm.nB1 : itm.nA1);
+      const int nX = COARSE ? 0x7fffffff : (x ? itm.nB : itm.nA);
       const int qb = x ? itm.qbB : itm.qbA;
       float m_used = -INFINITY, l = 0.f;  // P = 2^(s * scale - m_used), l = sum of this thread's P
-      for (int t = 0; t < nX; ++t) {
+      int t = 0;
+      for (; COARSE ? !crow.done() : t < nX; ++t) {
+        int cmask = 15;
+        const int cm = COARSE ? crow.next(cmask) : 0;
+        const bool diag = COARSE ? cm == qb : t == nX - 1;
         const int ph = (T + t) & 1;  // this tile's phase of s_full / p_lo / p_full
         FP_T8(6);
         mbar_wait(&sm.s_full[x], ph);
@@ -633,10 +731,21 @@ __global__ void __launch_bounds__(kThreads8, 1)
         const bool pv_ok = t == 0 || mbar_try_wait(smem_u32(&sm.pv_done[x]), (T + t - 1) & 1);
         tmem_wait_ld();
         FP_T8(1);
-        if (t == nX - 1) {  // the diagonal block: keys j <= r only
+        if (diag) {  // the diagonal block: keys j <= r only
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c > r) v[c] = -INFINITY;
+        }
+        if (COARSE) {  // unselected 64 x 64 quadrants of this warp's 64-row half (warp-uniform)
+          const int hx = r >> 6;
+          if (!((cmask >> (2 * hx)) & 1)) {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) v[c] = -INFINITY;
+          }
+          if (!((cmask >> (2 * hx + 1)) & 1)) {
+#pragma unroll
+            for (int c = 64; c < 128; ++c) v[c] = -INFINITY;
+          }
         }
         if (!pv_ok) mbar_wait(&sm.pv_done[x], (T + t - 1) & 1);
         // Tiles after a row's first: no row-max pass (64 fmax3 per row and
@@ -652,7 +761,9 @@ __global__ void __launch_bounds__(kThreads8, 1)
         // redone max-first (kExact8) by this CTA. Max-first: a row's first
         // tile and every tile of a redone item; the reference moves to the
         // max if it grew by > 2^8.
-        const bool fast = t > 0 && !exact;
+        // COARSE: a thread whose first tiles were all masked has no reference
+        // yet (m_used = -inf): its warp stays max-first until every lane has one
+        const bool fast = t > 0 && !exact && (!COARSE || __all_sync(0xffffffffu, m_used > -INFINITY));
         float alpha = 1.f;
         if (!fast) {
           // row max of the raw scores: 8 independent fmax3 chains, then a tree
@@ -686,7 +797,8 @@ __global__ void __launch_bounds__(kThreads8, 1)
             }
           }
         }
-        const float nm = -m_used;
+        // (a lane with no visible key so far: P = 2^-inf = 0)
+        const float nm = COARSE && m_used == -INFINITY ? 0.f : -m_used;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
@@ -728,11 +840,12 @@ __global__ void __launch_bounds__(kThreads8, 1)
         ++tacc[15];
 #endif
       }
+      const int ntl = t;  // tiles of this row in this item
       // overflow hazard of this row's P (checked on its row sum)
-      const bool flag = __any_sync(0xffffffffu, !exact && nX > 1 && !(l <= kGuard8));
-      if (nX > 0) {
+      const bool flag = __any_sync(0xffffffffu, !exact && ntl > 1 && !(l <= kGuard8));
+      if (ntl > 0) {
         // epilogue: O / l -> bf16 -> global (rows past n are not stored)
-        mbar_wait(&sm.pv_done[x], (T + nX - 1) & 1);
+        mbar_wait(&sm.pv_done[x], (T + ntl - 1) & 1);
         tc_fence_after();
         const float il = 1.0f / l;
         const int row = qb * 128 + r;
@@ -765,7 +878,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
         }
         tc_fence_before();  // O reads complete before P of the next item is released
       }
-      T += nX;
+      T += ntl;
       // a flagged item goes on the redo ring (once per item: the flag of its
       // slot dedupes the warps / rows that flag it), then the warp reports
       // the item done
@@ -803,13 +916,19 @@ extern "C" int fp_debug_attn8_timing(unsigned long long* out, int reset) {
 }
 #endif
 
+// s: the 128-block shape (items = H * ceil(nb / 2) q-tile pairs). coarse: the
+// CSR is a 64-block CSR of nb64 rows (capacity cap64 per head) walked as coarse
+// 128 x 128 tiles with quadrant masks (block size 64, see CoarseRow).
 cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap& qmap,
                            const CUtensorMap& kmap, const CUtensorMap& vmap, void* o,
-                           const int32_t* row_ptr, const int32_t* col_idx, bool dense,
-                           const void* const* peer_o, int n_peer, int* sched, cudaStream_t st) {
+                           const int32_t* row_ptr, const int32_t* col_idx, bool dense, bool coarse,
+                           int nb64, long long cap64, const void* const* peer_o, int n_peer, int* sched,
+                           cudaStream_t st) {
   const size_t smem = attn8_smem_bytes();
-  cudaError_t ea = ensure_smem_attr((const void*)attn8_kernel<true>, smem);
-  if (ea == cudaSuccess) ea = ensure_smem_attr((const void*)attn8_kernel<false>, smem);
+  cudaError_t ea = cudaSuccess;
+  for (const void* f : {(const void*)attn8_kernel<true, false>, (const void*)attn8_kernel<false, false>,
+                        (const void*)attn8_kernel<false, true>})
+    if (ea == cudaSuccess) ea = ensure_smem_attr(f, smem);
   if (ea != cudaSuccess) return ea;
   int dev = 0, nsm = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -828,14 +947,20 @@ cudaError_t launch_attn_v8(const Shape& s, const Layout& lay, const CUtensorMap&
   }
   auto* op = reinterpret_cast<__nv_bfloat16*>(o);
   const auto* po = reinterpret_cast<const unsigned long long*>(peer_o);
+  const long long cap = coarse ? cap64 : s.tri;
+  const int nbr = coarse ? nb64 : s.nb;
   if (dense)
-    FP_LAUNCH(attn8_kernel<true>, grid, kThreads8, smem, st, qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per, s.H,
-                                                      s.G, s.n, s.nb, s.tri, row_ptr, col_idx, scale_log2,
-                                                      po, n_peer, total, sched, order_gm);
+    FP_LAUNCH((attn8_kernel<true, false>), grid, kThreads8, smem, st, qmap, kmap, vmap, op, lay.o, lay.q.per,
+              lay.k.per, s.H, s.G, s.n, s.nb, cap, row_ptr, col_idx, scale_log2, po, n_peer, total, sched,
+              order_gm, nbr);
+  else if (coarse)
+    FP_LAUNCH((attn8_kernel<false, true>), grid, kThreads8, smem, st, qmap, kmap, vmap, op, lay.o, lay.q.per,
+              lay.k.per, s.H, s.G, s.n, s.nb, cap, row_ptr, col_idx, scale_log2, po, n_peer, total, sched,
+              order_gm, nbr);
   else
-    FP_LAUNCH(attn8_kernel<false>, grid, kThreads8, smem, st, qmap, kmap, vmap, op, lay.o, lay.q.per, lay.k.per,
-                                                       s.H, s.G, s.n, s.nb, s.tri, row_ptr, col_idx,
-                                                       scale_log2, po, n_peer, total, sched, order_gm);
+    FP_LAUNCH((attn8_kernel<false, false>), grid, kThreads8, smem, st, qmap, kmap, vmap, op, lay.o, lay.q.per,
+              lay.k.per, s.H, s.G, s.n, s.nb, cap, row_ptr, col_idx, scale_log2, po, n_peer, total, sched,
+              order_gm, nbr);
   return cudaGetLastError();
 }
 

@@ -2,7 +2,7 @@
 size ablation). The whole path runs with 64-token blocks: Q^ is the
 last 64 query rows, pooled estimates and line rasterisation use
 64-blocks, and the attention computes exactly the selected 64 x 64 blocks
-(fp_attn64.cu: coarse 128 x 128 tensor-core tiles with per-quadrant masks).
+(fp_attn8.cu: coarse 128 x 128 tensor-core tiles with per-quadrant masks).
 Parity against the float64 oracle run with b = 64."""
 import numpy as np
 import pytest
@@ -143,18 +143,22 @@ def test_block64_layer_host_matches_device_path(fp):
     assert np.array_equal(oh.float().numpy(), res["out"])
 
 
-def test_block64_peers_not_supported(fp):
-    """the fused output exchange is implemented by the b = 128 kernel only: the
-    b = 64 call fails loudly (FP_ERR_CUDA / cudaErrorNotSupported), nothing silent."""
+def test_block64_peers(fp):
+    """b = 64 runs the same (v8) attention kernel on coarse tiles, so the fused
+    output exchange works there too: every peer buffer receives exactly the
+    plain call's rows, bitwise."""
     import torch
     w = Workload("b64-peers", 4, 1, 1024, 0.9, 0.1, 0, 143)
     q, k, v = (parity.to_torch_bf16(x) for x in gen.make_layer_bits(w))
     fpl = fp.FlexPrefill(4, 1, 1024, block_size=B)
     fpl.plan(q, k, 0.1)
     fpl.select(0.9, 0)
+    ref = torch.zeros_like(q)
+    fpl.attn(q, k, v, ref)
     out = torch.zeros_like(q)
     peer = torch.zeros_like(q)
     ptrs = torch.tensor([peer.data_ptr()], dtype=torch.int64, device="cuda")
-    with pytest.raises(fp.FlexPrefillError):
-        fp.fp_sparse_attn_peers(q, k, v, out, ptrs, 1, 4, 1, 1024, fpl.row_ptr, fpl.col_idx,
-                                block_size=B)
+    fp.fp_sparse_attn_peers(q, k, v, out, ptrs, 1, 4, 1, 1024, fpl.row_ptr, fpl.col_idx,
+                            ws=fpl.ws, ws_bytes=fpl.ws_bytes, block_size=B)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref) and torch.equal(peer, ref)
