@@ -515,10 +515,10 @@ __global__ void __launch_bounds__(kThreads8, 1)
             for (;;) {
               if (redo_head < *vtail) {
                 // the pusher reserves its slot (tail) before writing it: wait
-                // for the entry, then free the slot (-1)
-                volatile int* slot = &sm.redo[redo_head++ & 7];
-                while ((item = *slot) < 0) __nanosleep(32);
-                *slot = -1;
+                // for the entry, then free the slot (-1); atomics on both sides
+                int* slot = &sm.redo[redo_head++ & 7];
+                while ((item = atomicOr(slot, 0)) < 0) __nanosleep(32);
+                atomicExch(slot, -1);
                 item |= kExact8;
                 if (sched) atomicAdd(sched + 1, 1);
                 break;
@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
       // the item done
       if (lane_id() == 0) {
         if (flag && atomicOr(&sm.redo_flag[k & 7], 1u) == 0) {
-          *reinterpret_cast<volatile int*>(&sm.redo[atomicAdd(&sm.redo_tail, 1) & 7]) = item & ~kExact8;
+          atomicExch(&sm.redo[atomicAdd(&sm.redo_tail, 1) & 7], item & ~kExact8);
           __threadfence_block();  // the ring entry before the done count (rare: no fence otherwise)
         }
         atomicAdd(&sm.done_warps, 1);

@@ -162,3 +162,29 @@ def test_block64_peers(fp):
                             ws=fpl.ws, ws_bytes=fpl.ws_bytes, block_size=B)
     torch.cuda.synchronize()
     assert torch.equal(out, ref) and torch.equal(peer, ref)
+
+
+@pytest.mark.slow
+def test_block64_32k_sampled(fp):
+    """b = 64 at full size (Llama-like 32/8 at 32k, the coarse-tile path of the
+    v8 kernel): end-to-end parity on sampled heads of both patterns and sampled
+    64-row query blocks against the b = 64 oracle (pattern, sets with borderline
+    elements reported, outputs within the north-star tolerance)."""
+    from synth.configs import C2
+    w = C2
+    q, k, v = gen.make_layer_bits(w)
+    res = parity.run_gpu(fp, w, q, k, v, block_size=B)
+    nb = -(-w.seq_len // B)
+    for h in range(w.heads):  # whole-layer CSR properties: sorted rows, forced blocks
+        rp, ci = res["row_ptr"][h], res["col_idx"][h]
+        assert rp[0] == 0 and np.all(np.diff(rp) >= np.minimum(np.arange(nb) + 1, 2))
+    heads = [0, 3]  # a Vertical-Slash-type and a Query-Aware-type head (synth/gen.py)
+    qbs = sorted({0, 1, 2, 3, nb // 2, nb // 2 + 1, nb - 2, nb - 1})
+    pats = set()
+    for h in heads:
+        g = h * w.kv_heads // w.heads
+        rep = parity.head_report(w, h, res, gen.bits_to_f64(q[h]), gen.bits_to_f64(k[g]),
+                                 gen.bits_to_f64(v[g]), qbs, b=B)
+        parity.check_report(rep)
+        pats.add(rep["pattern_oracle"])
+    assert pats == {0, 1}
