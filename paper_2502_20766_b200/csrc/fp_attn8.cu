@@ -86,10 +86,6 @@ constexpr float kGuard8 = 18446744073709551616.0f;
 // period is bound by its single S buffer (S(e+1) waits for softmax(e) and
 // PV(e)): the MMA pipeline alone runs at 3147 cycles per union entry against
 // 2048 of tensor work (the -DFP_XSM8 experiment), see DESIGN.md section 6.
-#ifndef FP_SPLIT8
-#define FP_SPLIT8 1
-#endif
-constexpr bool kSplit8 = FP_SPLIT8 != 0;
 
 struct Attn8Smem {
   uint8_t q[2][kTileBytes];  // Q_A, Q_B (1024-B aligned: first member)
@@ -141,42 +137,6 @@ FP_DEV void tmem_st_32x32b_x64_8(uint32_t taddr, const uint32_t* r) {
                : FP_W64(r), "r"(taddr));
 }
 
-// S = Q K^T, M=128 N=128, 8 k-steps of 16 in one asm statement, both operands
-// K-major SW128 tiles of two 16 KiB boxes in smem: k-step kk at box kk/4, byte
-// (kk%4)*32 (descriptor start-address offsets in 16-B units: 2, 4, 6, 1024...).
-FP_DEV void umma_ss_chain8(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %9, %17, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %10, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %11, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %12, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %5, %13, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %6, %14, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %7, %15, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %8, %16, %17, p;\n\t}" ::"r"(d),
-      "l"(a0), "l"(a0 + 2), "l"(a0 + 4), "l"(a0 + 6), "l"(a0 + 1024), "l"(a0 + 1026),
-      "l"(a0 + 1028), "l"(a0 + 1030), "l"(b0), "l"(b0 + 2), "l"(b0 + 4), "l"(b0 + 6),
-      "l"(b0 + 1024), "l"(b0 + 1026), "l"(b0 + 1028), "l"(b0 + 1030), "r"(idesc));
-}
-// O += P V, M=128 N=128, 8 k-steps (16 keys each): A = P in TMEM columns
-// a0 + 8 kk, B = V (MN-major SW128) descriptor b0 + kk * 2048 B.
-FP_DEV void umma_pv_chain8(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %18, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %9, %17, q;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %10, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %11, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %12, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %13, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %14, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %15, %17, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %16, %17, p;\n\t}" ::"r"(d),
-      "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "r"(a0 + 32), "r"(a0 + 40), "r"(a0 + 48),
-      "r"(a0 + 56), "l"(b0), "l"(b0 + 128), "l"(b0 + 256), "l"(b0 + 384), "l"(b0 + 512),
-      "l"(b0 + 640), "l"(b0 + 768), "l"(b0 + 896), "r"(idesc), "r"(acc0));
-}
-
 // The MMA issuer runs as a whole warp (FP_WARPISSUE8, default): every lane
 // executes the same loop on the same (warp-uniform) values and the MMA /
 // commit instructions are predicated on elect.sync inside the asm. With the
@@ -184,10 +144,6 @@ FP_DEV void umma_pv_chain8(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc,
 // per-thread registers and ptxas wraps every tcgen05.mma in an R2UR +
 // elect/branch loop: ~52 cycles to issue one MMA (tools/attn8_timing.py),
 // which made the single issuing thread the bottleneck of the kernel.
-#ifndef FP_WARPISSUE8
-#define FP_WARPISSUE8 1
-#endif
-constexpr bool kWarpIssue8 = FP_WARPISSUE8 != 0;
 #define FP_ELECT "elect.sync _|ep, 0xffffffff;\n\t"
 FP_DEV void umma_ss_chain8_w(uint32_t d, uint64_t a0, uint64_t b0, uint32_t idesc) {
   asm volatile(
@@ -221,21 +177,9 @@ FP_DEV void umma_commit_w(uint64_t* bar) {
       : "memory");
 }
 
-// Half of O += P V: 4 k-steps (64 keys) starting at P column a0 / V descriptor b0.
-FP_DEV void umma_pv_chain4(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, 1, 0;\n\tsetp.ne.b32 q, %10, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %9, q;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %6, %9, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %7, %9, p;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %8, %9, p;\n\t}" ::"r"(d),
-      "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "l"(b0), "l"(b0 + 128), "l"(b0 + 256),
-      "l"(b0 + 384), "r"(idesc), "r"(acc0));
-}
-
-#define PVCHAIN4(...) (kWarpIssue8 ? umma_pv_chain4_w(__VA_ARGS__) : umma_pv_chain4(__VA_ARGS__))
-#define SSCHAIN8(...) (kWarpIssue8 ? umma_ss_chain8_w(__VA_ARGS__) : umma_ss_chain8(__VA_ARGS__))
-#define COMMIT8(b) (kWarpIssue8 ? umma_commit_w(b) : umma_commit(b))
+#define PVCHAIN4(...) umma_pv_chain4_w(__VA_ARGS__)
+#define SSCHAIN8(...) umma_ss_chain8_w(__VA_ARGS__)
+#define COMMIT8(b) umma_commit_w(b)
 
 // Merge of the two rows' sorted key-block lists: next union entry.
 // mask bit 0: row A selected it, bit 1: row B. The list heads are loaded one
@@ -563,14 +507,6 @@ __global__ void __launch_bounds__(kThreads8, 1)
             const int kb = un.next(mask);
             const int s = e % depth;
             if (e >= depth) mbar_wait(&empty[s], ((e - depth) / depth) & 1);
-#ifdef FP_XNOTMA8
-            // experiment: after the ring's first fill, reuse the stale tiles
-            // (measures the kernel without L2 -> smem traffic; wrong results)
-            if (e >= depth) {
-              mbar_arrive(&full[s]);
-              continue;
-            }
-#endif
             mbar_arrive_expect_tx(&full[s], kTileBytes);
             tma_tile_hint(isK ? sm.k[s] : sm.v[s], map, &full[s], kb * 128, it.g, Gp, pol);
           }
@@ -581,7 +517,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
       }
     } else if (wid == 9) {
       // ------------------------------------------------ MMA issuer
-      if (kWarpIssue8 || lane_id() == 0) {
+      {  // the whole warp (elect.sync inside the MMA / commit asm)
         constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false);
         constexpr uint32_t idesc_o = make_idesc_bf16(128, 128, true);
         const uint64_t qdesc[2] = {sdesc_kmajor(smem_u32(sm.q[0]), 0), sdesc_kmajor(smem_u32(sm.q[1]), 0)};
@@ -603,27 +539,20 @@ __global__ void __launch_bounds__(kThreads8, 1)
             mbar_wait(&sm.v_full[vs], (ep / kVS8) & 1);
             FP_T8(9);
             const uint64_t vdesc = sdesc_mnmajor(smem_u32(sm.v[vs]), 0);
-            if (kSplit8) {
-              mbar_wait(&sm.p_lo[x], (cnt[x] - 1) & 1);
-              FP_T8(10);
-              tc_fence_after();
-              PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o, lcnt[x] > 1);
-              FP_T8(12);
-              mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
-              FP_T8(11);
+            mbar_wait(&sm.p_lo[x], (cnt[x] - 1) & 1);
+            FP_T8(10);
+            tc_fence_after();
+            PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o, lcnt[x] > 1);
+            FP_T8(12);
+            mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
+            FP_T8(11);
 #ifdef FP_TIMING
-              if (t_on) {
-                tacc[16] += clock64() - *(volatile long long*)&g_attn8_ts[blockIdx.x * 4 + x];
-              }
-#endif
-              tc_fence_after();
-              PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512, idesc_o, 1);
-            } else {
-              mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
-              tc_fence_after();
-              umma_pv_chain8(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o,
-                             lcnt[x] > 1);
+            if (t_on) {
+              tacc[16] += clock64() - *(volatile long long*)&g_attn8_ts[blockIdx.x * 4 + x];
             }
+#endif
+            tc_fence_after();
+            PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512, idesc_o, 1);
             COMMIT8(&sm.v_empty[vs]);
             COMMIT8(&sm.pv_done[x]);
             pend[x] = -1;
@@ -649,9 +578,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
               if (pend[x] >= 0) issue_pv(x);
               if (mask & (1 << x)) {
                 FP_T8(12);
-#if !defined(FP_XMMA8) && !defined(FP_XS8)
                 SSCHAIN8(tbase + kColS8 + x * 128, qdesc[x], kdesc, idesc_s);
-
                 FP_T8(13);  // issue time of the 8 S MMAs
                 COMMIT8(&sm.s_full[x]);
 #ifdef FP_TIMING
@@ -662,7 +589,6 @@ __global__ void __launch_bounds__(kThreads8, 1)
                 ++lcnt[x];
               }
             }
-#endif
             COMMIT8(&sm.k_empty[ks]);
             // an entry only one row uses gets its second V-slot release here
             // (it arrives early, but the phase also needs the PV's commit)
