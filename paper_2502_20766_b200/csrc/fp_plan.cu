@@ -434,8 +434,11 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
     FP_LAUNCH(pooled_softmax, dim3(s.nb, hy), kMapThreads, 0, sq, qa_only, s.H, s.nb, wsp<float>(ws, L.A_bar));
   };
   chk(launch_rep(s, qmap, kmap, Hp, Gp, scale_log2, m_part, l_part, nullptr, nullptr, nullptr, nullptr, 1, st));
-  FP_LAUNCH(rep_stats, s.H, 128, 0, st, s.nchunks, 128 - s.b, m_part, l_part, m_row, mp_row);
-  chk(launch_rep(s, qmap, kmap, Hp, Gp, scale_log2, nullptr, nullptr, mp_row, wsp<float>(ws, L.k_bar),
+  // few chunks: pass 2 combines the row statistics itself (one launch less);
+  // many: rep_stats once per head (every pass-2 CTA would re-read nchunks x 128 x 2)
+  const bool fold = s.nchunks <= 32;
+  if (!fold) FP_LAUNCH(rep_stats, s.H, 128, 0, st, s.nchunks, 128 - s.b, m_part, l_part, m_row, mp_row);
+  chk(launch_rep(s, qmap, kmap, Hp, Gp, scale_log2, fold ? m_part : nullptr, fold ? l_part : nullptr, mp_row, wsp<float>(ws, L.k_bar),
                  wsp<float>(ws, L.a_v), wsp<float>(ws, L.as_part), 2, st));
   if (side) {
     chk(cudaEventRecord(e_kbar, st));
