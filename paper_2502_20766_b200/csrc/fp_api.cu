@@ -158,10 +158,10 @@ size_t fp_col_idx_capacity(int seq_len, int block_size) {
   return nb * (nb + 1) / 2;
 }
 
-// fp_plan 9 (rep1, rep_stats, rep2, slash_combine, block_sums, pattern, qbar,
-// pooled_logits, pooled_softmax), fp_select 5 (topmass, build_lines,
-// assemble_rows, row_scan, write_cols), fp_sparse_attn 1
-int fp_kernels_per_layer(void) { return 9 + 5 + 1; }
+// at most: fp_plan 8 (rep1, rep_stats -- folded into rep2 when n <= 32k --,
+// rep2, line_sums, pattern, qbar, pooled_logits, pooled_softmax), fp_select 5
+// (topmass, build_lines, assemble_rows, row_scan, write_cols), fp_sparse_attn 1
+int fp_kernels_per_layer(void) { return 8 + 5 + 1; }
 
 fp_status fp_plan(const void* q, const void* k, int heads, int kv_heads, int seq_len, int head_dim,
                   int block_size, float tau, void* ws, size_t ws_bytes, int32_t* pattern,

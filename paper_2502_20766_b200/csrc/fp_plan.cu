@@ -7,11 +7,12 @@
 //   rep1_kernel   N1a  (fp_rep.cu) S = Q^ K^T per (key chunk, KV group, <= 4
 //                      heads) on tcgen05 -> partial row max / sum-exp
 //   rep_stats         combine partials -> per-row max and M' = max + log2(sum)
+//                     (n <= 32k: done by the rep2 CTAs themselves)
 //   rep2_kernel   N1b  (fp_rep.cu) S^T = K Q^T per (key chunk, KV group, <= 2
 //                      heads) -> p, a_v (column sums), per-tile slash
 //                      partials; the first subset of a group writes K_bar
-//   slash_combine     a_s[o] from the overlapping tile partials (fixed order)
-//   block_sums        a_hat[kb] = sum of a_v over kb (A2); As[D] (A12)
+//   line_sums         a_s[o] from the overlapping tile partials (fixed order),
+//                     a_hat[kb] = sum of a_v over kb (A2), As[D] (A12)
 //   pattern_kernel N3 a_bar = softmax(avgpool(Q^) K_bar^T / sqrt d), D_JS, decision
 //   qbar_kernel   N4a avg-pooled Q per block (QA heads only)
 //   pooled_logits N4b block-causal pooled logits, 32x32 tiles (QA heads only)
@@ -102,36 +103,34 @@ __global__ void rep_stats(int nchunks, int r_lo, const float* __restrict__ m_par
   mp_row[h * 128 + r] = r < r_lo ? INFINITY : m + log2f(l);
 }
 
-// a_s[o] = (sum of the overlapping per-tile diagonal partials) / b  (A9)
-__global__ void slash_combine(int n, int nt, float inv_b, const float* __restrict__ as_part,
-                              float* __restrict__ a_s) {
-  FP_PDL_ENTRY();
-  const int h = blockIdx.y;
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= n) return;
-  const int q = n - 128 - o;  // base(kt) = n - 128 - 128 kt ; delta = o - base = 128 kt - q
-  int kt_hi = (q + 127) >= 0 ? (q + 127) / 128 : -1;
-  float s = 0.f;
-  for (int kt = kt_hi - 1; kt <= kt_hi; ++kt) {  // ascending kt
-    if (kt < 0 || kt >= nt) continue;
-    const int delta = 128 * kt - q;
-    if (delta < -127 || delta > 127) continue;
-    s += as_part[((size_t)h * nt + kt) * 256 + delta + 127];
-  }
-  a_s[(size_t)h * n + o] = s * inv_b;
-}
-
-// a_hat[kb] = sum_{j in kb} a_v[j] (A2) and As[D] = sum_{o in block D} a_s[o] (A12)
-__global__ void block_sums(int n, int nb, int b, const float* __restrict__ a_v,
-                           const float* __restrict__ a_s, float* __restrict__ a_hat,
-                           float* __restrict__ As) {
+// One CTA per (key block kb, head): the slash scores of the block's offsets
+// a_s[o] = (sum of the overlapping per-tile diagonal partials) / b (A9), then
+// a_hat[kb] = sum_{j in kb} a_v[j] (A2) and As[kb] = sum_{o in block kb} a_s[o]
+// (A12) -- one launch for what were two kernels (slash combine, block sums).
+__global__ void line_sums(int n, int nt, int nb, int b, float inv_b, const float* __restrict__ as_part,
+                          const float* __restrict__ a_v, float* __restrict__ a_s, float* __restrict__ a_hat,
+                          float* __restrict__ As) {
   FP_PDL_ENTRY();
   __shared__ float red[33];
   const int kb = blockIdx.x, h = blockIdx.y;
-  const size_t i = (size_t)h * n + (size_t)kb * b + threadIdx.x;
-  const bool in = (int)threadIdx.x < b && kb * b + (int)threadIdx.x < n;  // ragged last block (A26)
-  float sv = block_sum<128>(in ? a_v[i] : 0.f, red);
-  float ss = block_sum<128>(in ? a_s[i] : 0.f, red);
+  const int o = kb * b + (int)threadIdx.x;
+  const bool in = (int)threadIdx.x < b && o < n;  // ragged last block (A26)
+  float as = 0.f;
+  if (in) {
+    const int q = n - 128 - o;  // base(kt) = n - 128 - 128 kt ; delta = o - base = 128 kt - q
+    const int kt_hi = (q + 127) >= 0 ? (q + 127) / 128 : -1;
+    float sum = 0.f;
+    for (int kt = kt_hi - 1; kt <= kt_hi; ++kt) {  // ascending kt
+      if (kt < 0 || kt >= nt) continue;
+      const int delta = 128 * kt - q;
+      if (delta < -127 || delta > 127) continue;
+      sum += as_part[((size_t)h * nt + kt) * 256 + delta + 127];
+    }
+    as = sum * inv_b;
+    a_s[(size_t)h * n + o] = as;
+  }
+  const float sv = block_sum<128>(in ? a_v[(size_t)h * n + o] : 0.f, red);
+  const float ss = block_sum<128>(in ? as : 0.f, red);
   if (threadIdx.x == 0) {
     a_hat[(size_t)h * nb + kb] = sv;
     As[(size_t)h * nb + kb] = ss;
@@ -445,12 +444,9 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
     pooled_map();
     chk(cudaEventRecord(e_join, side));
   }
-  FP_LAUNCH(slash_combine, dim3((s.n + 255) / 256, s.H), 256, 0, st, s.n, s.nt, 1.0f / (float)s.b,
-                                                              wsp<float>(ws, L.as_part),
-                                                              wsp<float>(ws, L.a_s));
-  FP_LAUNCH(block_sums, dim3(s.nb, s.H), 128, 0, st, s.n, s.nb, s.b, wsp<float>(ws, L.a_v),
-                                              wsp<float>(ws, L.a_s), wsp<float>(ws, L.a_hat),
-                                              wsp<float>(ws, L.As));
+  FP_LAUNCH(line_sums, dim3(s.nb, s.H), 128, 0, st, s.n, s.nt, s.nb, s.b, 1.0f / (float)s.b,
+            wsp<float>(ws, L.as_part), wsp<float>(ws, L.a_v), wsp<float>(ws, L.a_s), wsp<float>(ws, L.a_hat),
+            wsp<float>(ws, L.As));
   const size_t psm = (128 + 512 + (size_t)s.nb + 33) * 4;
   FP_LAUNCH(pattern_kernel, s.H, kPatThreads, psm, st, 
       reinterpret_cast<const __nv_bfloat16*>(q), lay.q, wsp<float>(ws, L.k_bar), wsp<float>(ws, L.a_hat),
