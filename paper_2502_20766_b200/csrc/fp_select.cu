@@ -567,17 +567,14 @@ __global__ void __launch_bounds__(kRowThreads) topmass_rows(
   }
 }
 
-// vertical-block and slash-diagonal bitmaps of VS heads (A10, reading R1)
-__global__ void build_lines(const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_v,
-                            const int32_t* __restrict__ sel_s, const int32_t* __restrict__ sel_count,
-                            int n, int nb, int nbw, int vs_mode, int lb, uint32_t* __restrict__ vbits,
-                            uint32_t* __restrict__ dbits) {
-  FP_PDL_ENTRY();
-  extern __shared__ uint32_t bsm[];  // V[nbw] | D[nbw]
-  const int h = blockIdx.x;
-  uint32_t* V = bsm;
-  uint32_t* Dg = bsm + nbw;
-  for (int w = threadIdx.x; w < 2 * nbw; w += blockDim.x) bsm[w] = 0;
+// vertical-block and slash-diagonal bitmaps of VS heads (A10, reading R1):
+// V / Dg are this CTA's shared-memory bitmaps (nbw words each), also stored
+// to vbits / dbits. All threads of the CTA call it.
+__device__ void build_lines_body(int h, uint32_t* V, uint32_t* Dg, const int32_t* __restrict__ pattern,
+                                 const int32_t* __restrict__ sel_v, const int32_t* __restrict__ sel_s,
+                                 const int32_t* __restrict__ sel_count, int n, int nb, int nbw, int vs_mode,
+                                 int lb, uint32_t* __restrict__ vbits, uint32_t* __restrict__ dbits) {
+  for (int w = threadIdx.x; w < nbw; w += blockDim.x) V[w] = Dg[w] = 0;
   __syncthreads();
   if (pattern[h] == 0) {
     const int kv = sel_count[h * 4 + 0], ks = sel_count[h * 4 + 1];
@@ -602,31 +599,34 @@ __global__ void build_lines(const int32_t* __restrict__ pattern, const int32_t* 
     dbits[(size_t)h * nbw + w] = Dg[w];
   }
 }
+__global__ void build_lines(const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_v,
+                            const int32_t* __restrict__ sel_s, const int32_t* __restrict__ sel_count,
+                            int n, int nb, int nbw, int vs_mode, int lb, uint32_t* __restrict__ vbits,
+                            uint32_t* __restrict__ dbits) {
+  FP_PDL_ENTRY();
+  extern __shared__ uint32_t bsm[];  // V[nbw] | D[nbw]
+  build_lines_body(blockIdx.x, bsm, bsm + nbw, pattern, sel_v, sel_s, sel_count, n, nb, nbw, vs_mode, lb,
+                   vbits, dbits);
+}
 
 __device__ __forceinline__ bool bit_at(const uint32_t* b, int i) { return (b[i >> 5] >> (i & 31)) & 1u; }
 
 // one warp per (head, query-block row)
 constexpr int kAsmWarps = 8;
-__global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows(
-    const int32_t* __restrict__ pattern, const uint32_t* __restrict__ vbits,
-    const uint32_t* __restrict__ dbits, const int32_t* __restrict__ sel_qa,
-    const int32_t* __restrict__ sel_count, const float* __restrict__ a_hat,
-    const float* __restrict__ As, const float* __restrict__ A_bar, int nb, int nbw,
-    long long tri, int min_blocks, int qa_mode, const uint32_t* __restrict__ selbits,
-    int max_blocks, uint32_t* __restrict__ rowbits, int32_t* __restrict__ row_nnz,
-    int32_t* __restrict__ row_nnz_pre, int32_t* __restrict__ budget_added,
-    int32_t* __restrict__ budget_removed) {
-  FP_PDL_ENTRY();
-  extern __shared__ uint32_t asmem[];  // [kAsmWarps][2][nbw]
-  const int h = blockIdx.y;
-  const int w = warp_id(), ln = lane_id();
-  const int qb = blockIdx.x * kAsmWarps + w;
-  if (qb >= nb) return;
-  uint32_t* row = asmem + w * 2 * nbw;
-  uint32_t* keep = row + nbw;
+// One query-block row qb of head h, by one warp: rasterised lines or QA
+// blocks, forced blocks (A11), minimum / maximum budget (A12, A23); row / keep
+// are the warp's nbw-word scratch, V / Dg the head's line bitmaps.
+__device__ void assemble_row(int h, int qb, uint32_t* row, uint32_t* keep, const uint32_t* V,
+                             const uint32_t* Dg, const int32_t* __restrict__ pattern,
+                             const int32_t* __restrict__ sel_qa, const int32_t* __restrict__ sel_count,
+                             const float* __restrict__ a_hat, const float* __restrict__ As,
+                             const float* __restrict__ A_bar, int nb, int nbw, long long tri, int min_blocks,
+                             int qa_mode, const uint32_t* __restrict__ selbits, int max_blocks,
+                             uint32_t* __restrict__ rowbits, int32_t* __restrict__ row_nnz,
+                             int32_t* __restrict__ row_nnz_pre, int32_t* __restrict__ budget_added,
+                             int32_t* __restrict__ budget_removed) {
+  const int ln = lane_id();
   const int pat = pattern[h];
-  const uint32_t* V = vbits + (size_t)h * nbw;
-  const uint32_t* Dg = dbits + (size_t)h * nbw;
   for (int i = ln; i < nbw; i += 32) row[i] = 0;
   __syncwarp();
   const int nw_row = (qb >> 5) + 1;  // words that can hold kb <= qb
@@ -746,16 +746,36 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows(
   }
 }
 
-// exclusive scan of row nnz per head -> row_ptr; stats
-__global__ void __launch_bounds__(kSelThreads, 1)
-    row_scan(const int32_t* __restrict__ row_nnz, const int32_t* __restrict__ budget_added,
-             const int32_t* __restrict__ budget_removed,
-             const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_count,
-             const unsigned long long* __restrict__ sel_mass, int nb, int32_t* __restrict__ row_ptr,
-             fp_select_stats* __restrict__ stats) {
+__global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows(
+    const int32_t* __restrict__ pattern, const uint32_t* __restrict__ vbits,
+    const uint32_t* __restrict__ dbits, const int32_t* __restrict__ sel_qa,
+    const int32_t* __restrict__ sel_count, const float* __restrict__ a_hat,
+    const float* __restrict__ As, const float* __restrict__ A_bar, int nb, int nbw,
+    long long tri, int min_blocks, int qa_mode, const uint32_t* __restrict__ selbits,
+    int max_blocks, uint32_t* __restrict__ rowbits, int32_t* __restrict__ row_nnz,
+    int32_t* __restrict__ row_nnz_pre, int32_t* __restrict__ budget_added,
+    int32_t* __restrict__ budget_removed) {
   FP_PDL_ENTRY();
-  __shared__ uint64_t wsum[32];
-  const int h = blockIdx.x;
+  extern __shared__ uint32_t asmem[];  // [kAsmWarps][2][nbw]
+  const int h = blockIdx.y;
+  const int w = warp_id();
+  const int qb = blockIdx.x * kAsmWarps + w;
+  if (qb >= nb) return;
+  uint32_t* row = asmem + w * 2 * nbw;
+  assemble_row(h, qb, row, row + nbw, vbits + (size_t)h * nbw, dbits + (size_t)h * nbw, pattern, sel_qa,
+               sel_count, a_hat, As, A_bar, nb, nbw, tri, min_blocks, qa_mode, selbits, max_blocks, rowbits,
+               row_nnz, row_nnz_pre, budget_added, budget_removed);
+}
+
+// exclusive scan of row nnz per head -> row_ptr; stats
+// exclusive scan of row nnz of head h -> row_ptr; stats (all threads of a
+// kSelThreads CTA; wsum: 32 words of shared scratch)
+__device__ void row_scan_body(int h, uint64_t* wsum, const int32_t* __restrict__ row_nnz,
+                              const int32_t* __restrict__ budget_added,
+                              const int32_t* __restrict__ budget_removed, const int32_t* __restrict__ pattern,
+                              const int32_t* __restrict__ sel_count,
+                              const unsigned long long* __restrict__ sel_mass, int nb,
+                              int32_t* __restrict__ row_ptr, fp_select_stats* __restrict__ stats) {
   uint64_t run = 0, badd = 0, brem = 0;
   for (int base = 0; base < nb; base += kSelThreads) {
     const int i = base + threadIdx.x;
@@ -791,14 +811,22 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   }
 }
 
-__global__ void __launch_bounds__(kAsmWarps * 32) write_cols(
-    const uint32_t* __restrict__ rowbits, const int32_t* __restrict__ row_ptr, int nb, int nbw,
-    long long cap, int32_t* __restrict__ col_idx) {
+__global__ void __launch_bounds__(kSelThreads, 1)
+    row_scan(const int32_t* __restrict__ row_nnz, const int32_t* __restrict__ budget_added,
+             const int32_t* __restrict__ budget_removed,
+             const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_count,
+             const unsigned long long* __restrict__ sel_mass, int nb, int32_t* __restrict__ row_ptr,
+             fp_select_stats* __restrict__ stats) {
   FP_PDL_ENTRY();
-  const int h = blockIdx.y;
-  const int w = warp_id(), ln = lane_id();
-  const int qb = blockIdx.x * kAsmWarps + w;
-  if (qb >= nb) return;
+  __shared__ uint64_t wsum[32];
+  row_scan_body(blockIdx.x, wsum, row_nnz, budget_added, budget_removed, pattern, sel_count, sel_mass, nb,
+                row_ptr, stats);
+}
+
+// the CSR column indices of row qb of head h (ascending kb), by one warp
+__device__ void write_row(int h, int qb, const uint32_t* __restrict__ rowbits, const int32_t* __restrict__ row_ptr,
+                          int nb, int nbw, long long cap, int32_t* __restrict__ col_idx) {
+  const int ln = lane_id();
   const uint32_t* row = rowbits + ((size_t)h * nb + qb) * nbw;
   int32_t* out = col_idx + (size_t)h * cap + row_ptr[(size_t)h * (nb + 1) + qb];
   int pos = 0;
@@ -808,6 +836,49 @@ __global__ void __launch_bounds__(kAsmWarps * 32) write_cols(
     if ((word >> ln) & 1u) out[pos + __popc(word & ((1u << ln) - 1u))] = wd * 32 + ln;
     pos += __popc(word);
   }
+}
+__global__ void __launch_bounds__(kAsmWarps * 32) write_cols(
+    const uint32_t* __restrict__ rowbits, const int32_t* __restrict__ row_ptr, int nb, int nbw,
+    long long cap, int32_t* __restrict__ col_idx) {
+  FP_PDL_ENTRY();
+  const int h = blockIdx.y;
+  const int qb = blockIdx.x * kAsmWarps + warp_id();
+  if (qb >= nb) return;
+  write_row(h, qb, rowbits, row_ptr, nb, nbw, cap, col_idx);
+}
+
+// Short sequences (nb <= kPostSmallNb): lines, rows, scan and columns of one
+// head in ONE CTA of kSelThreads (32 warps, each a stripe of rows) -- the same
+// device code as the four kernels above, so the same CSR, in one launch
+// instead of four (each of which costs its launch / ramp at this size).
+constexpr int kPostSmallNb = 64;
+__global__ void __launch_bounds__(kSelThreads, 1) select_post_small(
+    const int32_t* __restrict__ pattern, const int32_t* __restrict__ sel_v, const int32_t* __restrict__ sel_s,
+    const int32_t* __restrict__ sel_qa, const int32_t* __restrict__ sel_count,
+    const unsigned long long* __restrict__ sel_mass, const float* __restrict__ a_hat,
+    const float* __restrict__ As, const float* __restrict__ A_bar, int n, int nb, int nbw, long long tri,
+    int vs_mode, int lb, int min_blocks, int qa_mode, const uint32_t* __restrict__ selbits, int max_blocks,
+    uint32_t* __restrict__ vbits, uint32_t* __restrict__ dbits, uint32_t* __restrict__ rowbits,
+    int32_t* __restrict__ row_nnz, int32_t* __restrict__ row_nnz_pre, int32_t* __restrict__ budget_added,
+    int32_t* __restrict__ budget_removed, int32_t* __restrict__ row_ptr, fp_select_stats* __restrict__ stats,
+    int32_t* __restrict__ col_idx) {
+  FP_PDL_ENTRY();
+  __shared__ uint32_t V[kPostSmallNb / 32], Dg[kPostSmallNb / 32];
+  __shared__ uint32_t scr[kSelThreads / 32][2][kPostSmallNb / 32];
+  __shared__ uint64_t wsum[32];
+  const int h = blockIdx.x;
+  const int w = warp_id();
+  build_lines_body(h, V, Dg, pattern, sel_v, sel_s, sel_count, n, nb, nbw, vs_mode, lb, vbits, dbits);
+  __syncthreads();
+  for (int qb = w; qb < nb; qb += kSelThreads / 32)
+    assemble_row(h, qb, scr[w][0], scr[w][1], V, Dg, pattern, sel_qa, sel_count, a_hat, As, A_bar, nb, nbw,
+                 tri, min_blocks, qa_mode, selbits, max_blocks, rowbits, row_nnz, row_nnz_pre, budget_added,
+                 budget_removed);
+  __syncthreads();
+  row_scan_body(h, wsum, row_nnz, budget_added, budget_removed, pattern, sel_count, sel_mass, nb, row_ptr,
+                stats);
+  __syncthreads();
+  for (int qb = w; qb < nb; qb += kSelThreads / 32) write_row(h, qb, rowbits, row_ptr, nb, nbw, tri, col_idx);
 }
 
 }  // namespace
@@ -856,15 +927,25 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
     FP_LAUNCH(topmass_rows, dim3(s.nb, s.H), kRowThreads, 0, st, 
         wsp<float>(ws, L.A_bar), pat, s.nb, L.nbw, s.tri, gamma, wsp<uint32_t>(ws, L.selbits),
         wsp<int32_t>(ws, L.sel_count), wsp<unsigned long long>(ws, L.sel_mass));
+  // A12 / f2: budgets in tokens -> key blocks of this block size
+  // (int64: token budgets near INT_MAX must not overflow; clamped to nb)
+  const int min_blocks = (int)std::min<long long>(s.nb, ((long long)min_budget + s.b - 1) / s.b);
+  const int max_blocks = (int)std::min<long long>(s.nb, ((long long)opt.max_budget + s.b - 1) / s.b);
+  if (s.nb <= kPostSmallNb) {
+    FP_LAUNCH(select_post_small, s.H, kSelThreads, 0, st, pat, wsp<int32_t>(ws, L.sel_v), wsp<int32_t>(ws, L.sel_s),
+              wsp<int32_t>(ws, L.sel_qa), wsp<int32_t>(ws, L.sel_count), wsp<unsigned long long>(ws, L.sel_mass),
+              wsp<float>(ws, L.a_hat), wsp<float>(ws, L.As), wsp<float>(ws, L.A_bar), s.n, s.nb, L.nbw, s.tri,
+              opt.vs_mode, s.lb, min_blocks, opt.qa_mode, wsp<uint32_t>(ws, L.selbits), max_blocks,
+              wsp<uint32_t>(ws, L.vbits), wsp<uint32_t>(ws, L.dbits), wsp<uint32_t>(ws, L.rowbits),
+              wsp<int32_t>(ws, L.row_nnz), wsp<int32_t>(ws, L.row_nnz_pre), wsp<int32_t>(ws, L.budget_added),
+              wsp<int32_t>(ws, L.budget_removed), row_ptr, stats, col_idx);
+    return cudaGetLastError();
+  }
   FP_LAUNCH(build_lines, s.H, 1024, 2 * L.nbw * 4, st, pat, wsp<int32_t>(ws, L.sel_v),
                                                 wsp<int32_t>(ws, L.sel_s),
                                                 wsp<int32_t>(ws, L.sel_count), s.n, s.nb, L.nbw,
                                                 opt.vs_mode, s.lb, wsp<uint32_t>(ws, L.vbits),
                                                 wsp<uint32_t>(ws, L.dbits));
-  // A12 / f2: budgets in tokens -> key blocks of this block size
-  // (int64: token budgets near INT_MAX must not overflow; clamped to nb)
-  const int min_blocks = (int)std::min<long long>(s.nb, ((long long)min_budget + s.b - 1) / s.b);
-  const int max_blocks = (int)std::min<long long>(s.nb, ((long long)opt.max_budget + s.b - 1) / s.b);
   const dim3 rg((s.nb + kAsmWarps - 1) / kAsmWarps, s.H);
   FP_LAUNCH(assemble_rows, rg, kAsmWarps * 32, kAsmWarps * 2 * L.nbw * 4, st, 
       pat, wsp<uint32_t>(ws, L.vbits), wsp<uint32_t>(ws, L.dbits), wsp<int32_t>(ws, L.sel_qa),
