@@ -260,71 +260,126 @@ __global__ void __launch_bounds__(256) qbar_kernel(const __nv_bfloat16* __restri
 
 // A_bar[qb, kb <= qb] = softmax_row(scale * Qbar[qb] . Kbar[kb]) / nb  (A5)
 // Two kernels: pooled_logits computes the block-causal logits tile by tile
-// (32 x 32 block pairs per CTA, Qbar and Kbar tiles staged in shared memory,
-// fp32 FFMA dot products in fixed d order) straight into the packed A_bar
-// rows; pooled_softmax normalises each row in place.
-constexpr int kPT = 32;  // row / column tile of the pooled logits
-// grid (ntri, H): lower-triangle tile index -> (row tile rt, column tile ct <= rt);
-// 64 threads, each a 4 x 4 block of (qb, kb) logits, d in float4 steps
-__global__ void __launch_bounds__(64) pooled_logits(
+// (PT x PT block pairs per CTA, fp32 FFMA dot products in fixed d order
+// 0..127) straight into the packed A_bar rows; pooled_softmax normalises each
+// row in place.
+//
+// pooled_logits: grid (ntri, head ranges); lower-triangle tile index -> (row
+// tile rt, column tile ct <= rt). PT * PT / 16 threads, each a 4 x 4 block of
+// logits. The work of a CTA is a list of units (QA head of its range, half of
+// d); the Qbar / Kbar tiles of unit u + 1 are copied (cp.async, 16 B per
+// thread and row chunk) into the other of two shared buffers while unit u is
+// multiplied. Tiles are transposed [d / 4][row] with one float4 of padding per
+// d row (the copies of a warp -- consecutive d / 4 of one row, coalesced in
+// global memory -- land in distinct bank quads).
+constexpr int kPLMaxHeads = 64;  // heads per range (launch: H / gridDim.y <= 64)
+FP_DEV void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+FP_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+FP_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+template <int PT>
+constexpr size_t pooled_logits_smem() {
+  return sizeof(float4) * 2 * 2 * 16 * (PT + 1);
+}
+template <int PT>
+__global__ void __launch_bounds__(PT * PT / 16) pooled_logits(
     const float* __restrict__ q_bar, const float* __restrict__ k_bar,
     const int32_t* __restrict__ pattern, int H, int G, int nb, float scale,
     float* __restrict__ A_bar) {
+  constexpr int NT = PT * PT / 16;
   FP_PDL_ENTRY();
+  extern __shared__ float4 pl_smem[];  // [buffer][q / k][16][PT + 1]
+  __shared__ int qah[kPLMaxHeads];
+  __shared__ int nqa_s;
   const int h_lo = blockIdx.y * H / gridDim.y, h_hi = (blockIdx.y + 1) * H / gridDim.y;
   // triangular decode of blockIdx.x = rt (rt + 1) / 2 + ct
   int rt = (int)((sqrtf(8.0f * (float)blockIdx.x + 1.0f) - 1.0f) * 0.5f);
   while ((rt + 1) * (rt + 2) / 2 <= (int)blockIdx.x) ++rt;
   while (rt * (rt + 1) / 2 > (int)blockIdx.x) --rt;
   const int ct = (int)blockIdx.x - rt * (rt + 1) / 2;
-  // transposed float4 tiles [d / 4][row]: the 4 x 4 register tiles read 4 / 8
-  // consecutive float4s per warp instruction (conflict-free shared loads)
-  __shared__ float4 qs4[32][kPT];
-  __shared__ float4 ks4[32][kPT];
   const int tid = threadIdx.x;
-  for (int h = h_lo; h < h_hi; ++h) {
-  if (pattern && pattern[h] != 1) continue;
-  __syncthreads();  // the previous head's tiles are consumed
-  const int g = h / (H / G);
-  for (int e = tid; e < kPT * 32; e += 64) {
-    const int rr = e >> 5, d4 = e & 31;
-    const int qb = rt * kPT + rr, kb = ct * kPT + rr;
-    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-    qs4[d4][rr] = qb < nb ? __ldg(reinterpret_cast<const float4*>(q_bar + ((size_t)h * nb + qb) * 128) + d4) : zero;
-    ks4[d4][rr] = kb < nb ? __ldg(reinterpret_cast<const float4*>(k_bar + ((size_t)g * nb + kb) * 128) + d4) : zero;
+  if (tid == 0) {
+    int c = 0;
+    for (int h = h_lo; h < h_hi; ++h)
+      if (!pattern || pattern[h] == 1) qah[c++] = h;
+    nqa_s = c;
   }
   __syncthreads();
-  const int r0 = (tid >> 3) * 4, c0 = (tid & 7) * 4;
-  float acc[4][4] = {};
+  const int nu = 2 * nqa_s;
+  if (nu == 0) return;
+  auto buf = [&](int b, int qk, int d4, int row) -> float4* {
+    return pl_smem + ((b * 2 + qk) * 16 + d4) * (PT + 1) + row;
+  };
+  auto fill = [&](int u) {
+    const int h = qah[u >> 1], dh = u & 1, g = h / (H / G), b = u & 1;
+    for (int e = tid; e < PT * 16; e += NT) {
+      const int er = e >> 4, d4 = e & 15;
+      const int qb = rt * PT + er, kb = ct * PT + er;
+      cp_async16(buf(b, 0, d4, er), q_bar + ((size_t)h * nb + min(qb, nb - 1)) * 128 + (dh * 16 + d4) * 4, qb < nb);
+      cp_async16(buf(b, 1, d4, er), k_bar + ((size_t)g * nb + min(kb, nb - 1)) * 128 + (dh * 16 + d4) * 4, kb < nb);
+    }
+    cp_async_commit();
+  };
+  // rows rr + TPR i, columns cc + TPR j: a warp's Kbar reads are consecutive
+  // float4s (conflict-free), its A_bar stores consecutive kb
+  constexpr int TPR = PT / 4;
+  const int rr = tid / TPR, cc = tid % TPR;
+  float acc[4][4];
+  fill(0);
+  for (int u = 0; u < nu; ++u) {
+    if (u + 1 < nu) {
+      fill(u + 1);  // buffer (u + 1) & 1: consumed by unit u - 1 (barrier at its end)
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if ((u & 1) == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    }
+    const int b = u & 1;
 #pragma unroll 4
-  for (int d4 = 0; d4 < 32; ++d4) {
-    float4 qv[4], kv[4];
+    for (int d4 = 0; d4 < 16; ++d4) {
+      float4 qv[4], kv[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      qv[i] = qs4[d4][r0 + i];
-      kv[i] = ks4[d4][c0 + i];
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        acc[i][j] = fmaf(qv[i].x, kv[j].x, acc[i][j]);
-        acc[i][j] = fmaf(qv[i].y, kv[j].y, acc[i][j]);
-        acc[i][j] = fmaf(qv[i].z, kv[j].z, acc[i][j]);
-        acc[i][j] = fmaf(qv[i].w, kv[j].w, acc[i][j]);
+      for (int i = 0; i < 4; ++i) {
+        qv[i] = *buf(b, 0, d4, rr + TPR * i);
+        kv[i] = *buf(b, 1, d4, cc + TPR * i);
       }
-  }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int qb = rt * kPT + r0 + i;
-    if (qb >= nb) continue;
-    float* row = A_bar + (size_t)h * ((size_t)nb * (nb + 1) / 2) + (size_t)qb * (qb + 1) / 2;
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int kb = ct * kPT + c0 + j;
-      if (kb <= qb) row[kb] = acc[i][j] * scale;
+        for (int j = 0; j < 4; ++j) {
+          acc[i][j] = fmaf(qv[i].x, kv[j].x, acc[i][j]);
+          acc[i][j] = fmaf(qv[i].y, kv[j].y, acc[i][j]);
+          acc[i][j] = fmaf(qv[i].z, kv[j].z, acc[i][j]);
+          acc[i][j] = fmaf(qv[i].w, kv[j].w, acc[i][j]);
+        }
     }
-  }
+    __syncthreads();  // buffer b is free for unit u + 2
+    if (u & 1) {
+      const int h = qah[u >> 1];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int qb = rt * PT + rr + TPR * i;
+        if (qb >= nb) continue;
+        float* row = A_bar + (size_t)h * ((size_t)nb * (nb + 1) / 2) + (size_t)qb * (qb + 1) / 2;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int kb = ct * PT + cc + TPR * j;
+          if (kb <= qb) row[kb] = acc[i][j] * scale;
+        }
+      }
+    }
   }
 }
 
@@ -391,6 +446,11 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
   float* mp_row = wsp<float>(ws, L.mp_row);  // M'_r = m_r + log2 l_r
   (void)k;
   const int Hp = lay.q.per, Gp = lay.k.per;
+  {
+    cudaError_t ea = ensure_smem_attr((const void*)pooled_logits<64>, pooled_logits_smem<64>());
+    if (ea == cudaSuccess) ea = ensure_smem_attr((const void*)pooled_logits<32>, pooled_logits_smem<32>());
+    if (ea != cudaSuccess) return ea;
+  }
   // The Query-Aware pooled map (a3: q_bar, pooled logits, row softmax) needs
   // only Q and K_bar, not the pattern: it can run for EVERY head on a side stream,
   // concurrently with the second representative pass .. pattern_kernel, and is
@@ -415,10 +475,15 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
   }
   const int32_t* qa_only = side ? nullptr : wsp<int32_t>(ws, L.pattern);
   cudaStream_t sq = side ? side : st;
+  // 64 x 64 logit tiles from nb >= 256 (fewer, larger CTAs: half the tile
+  // traffic per logit); 32 x 32 at short n (more CTAs for few blocks)
+  const bool big_tiles = s.nb >= 256;
+  const int kPT = big_tiles ? 64 : 32;
   const int nt = (s.nb + kPT - 1) / kPT;
   // one CTA per head when every head is pooled (short n, side stream);
-  // otherwise CTAs over head ranges that skip the Vertical-Slash heads
-  const int hy = qa_only ? std::min(s.H, 4) : s.H;
+  // otherwise CTAs over head ranges (<= kPLMaxHeads heads) that skip the
+  // Vertical-Slash heads
+  const int hy = qa_only ? std::min(s.H, std::max(4, (s.H + kPLMaxHeads - 1) / kPLMaxHeads)) : s.H;
   if (side)  // q_bar does not need K_bar: start it at the fork
     FP_LAUNCH(qbar_kernel, dim3(s.nb, hy), 256, 0, sq, reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
                                                  qa_only, s.H, s.n, s.nb, s.b, wsp<float>(ws, L.q_bar));
@@ -427,9 +492,14 @@ cudaError_t launch_plan(const Shape& s, const WsLayout& L, void* ws, const void*
       FP_LAUNCH(qbar_kernel, dim3(s.nb, hy), 256, 0, sq, reinterpret_cast<const __nv_bfloat16*>(q), lay.q,
                                                    qa_only, s.H, s.n, s.nb, s.b, wsp<float>(ws, L.q_bar));
     if (side) chk(cudaStreamWaitEvent(side, e_kbar, 0));  // K_bar from the second pass
-    FP_LAUNCH(pooled_logits, dim3(nt * (nt + 1) / 2, hy), 64, 0, sq, wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar),
-                                                     qa_only, s.H, s.G, s.nb, scale,
-                                                     wsp<float>(ws, L.A_bar));
+    if (big_tiles)
+      FP_LAUNCH(pooled_logits<64>, dim3(nt * (nt + 1) / 2, hy), 256, pooled_logits_smem<64>(), sq,
+                wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar), qa_only, s.H, s.G, s.nb, scale,
+                wsp<float>(ws, L.A_bar));
+    else
+      FP_LAUNCH(pooled_logits<32>, dim3(nt * (nt + 1) / 2, hy), 64, pooled_logits_smem<32>(), sq,
+                wsp<float>(ws, L.q_bar), wsp<float>(ws, L.k_bar), qa_only, s.H, s.G, s.nb, scale,
+                wsp<float>(ws, L.A_bar));
     FP_LAUNCH(pooled_softmax, dim3(s.nb, hy), kMapThreads, 0, sq, qa_only, s.H, s.nb, wsp<float>(ws, L.A_bar));
   };
   chk(launch_rep(s, qmap, kmap, Hp, Gp, scale_log2, m_part, l_part, nullptr, nullptr, nullptr, nullptr, 1, st));

@@ -28,6 +28,9 @@ namespace fp {
 
 namespace {
 
+#ifndef FP_TOPMASS_AGG
+#define FP_TOPMASS_AGG 0  // 1: warp-aggregated histogram updates (round-2 kernel)
+#endif
 constexpr int kSelThreads = 1024;
 constexpr int kItems = 8;
 constexpr float kFixScale = 1152921504606846976.0f;  // 2^60
@@ -145,30 +148,69 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
       sm.mass[b] = 0;
     }
     __syncthreads();
-    // local histogram of the slice (warp-aggregated smem atomics), 4 loads in flight
-    for (long long base = lo; base < hi; base += 4 * kSelThreads) {
-      uint32_t keys[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long long i = base + u * kSelThreads + tid;
-        keys[u] = i < hi ? __float_as_uint(__ldg(x + i)) : 0xffffffffu;
+    // local histogram of the slice: 16-B loads of the 16-B-aligned body (4 in
+    // flight per thread = 16 keys), the <= 3 keys before / after it scalar
+    auto hist_key = [&](uint32_t key) {
+      const bool match = key != 0xffffffffu && ((key & pmask) == prefix);
+#if FP_TOPMASS_AGG
+      const uint32_t digit = match ? ((key >> sh) & dmask) : 0xffffffffu;
+      const uint32_t grp = __match_any_sync(__activemask(), digit);
+      if (match) {
+        const uint64_t f = fixp(__uint_as_float(key));
+        const uint32_t s0 = __reduce_add_sync(grp, (uint32_t)(f & 0xFFFFF));
+        const uint32_t s1 = __reduce_add_sync(grp, (uint32_t)((f >> 20) & 0xFFFFF));
+        const uint32_t s2 = __reduce_add_sync(grp, (uint32_t)(f >> 40));
+        if ((__ffs(grp) - 1) == (int)lane_id()) {
+          atomicAdd(&sm.cnt[digit], (uint32_t)__popc(grp));
+          atomicAdd(&sm.mass[digit], ((unsigned long long)s2 << 40) +
+                                         ((unsigned long long)s1 << 20) + (unsigned long long)s0);
+        }
       }
+#else
+      // shared atomics per matching key (integer: order independent) instead
+      // of aggregating same-digit lanes first (match + three partial-mask
+      // reductions, a loop over the warp's distinct digits): the count is a
+      // hardware-aggregated increment, the 64-bit mass two 32-bit adds on the
+      // halves of mass[digit] (little endian) with the carry of the low one
+      if (match) {
+        const uint32_t digit = (key >> sh) & dmask;
+        const uint64_t f = fixp(__uint_as_float(key));
+        uint32_t* mh = reinterpret_cast<uint32_t*>(&sm.mass[digit]);
+        atomicAdd(&sm.cnt[digit], 1u);
+        const uint32_t lo = (uint32_t)f;
+        const uint32_t old = atomicAdd(mh, lo);
+        const uint32_t hi = (uint32_t)(f >> 32) + (old + lo < old ? 1u : 0u);
+        if (hi) atomicAdd(mh + 1, hi);
+      }
+#endif
+    };
+    {
+      const long long xmis = (long long)((reinterpret_cast<uintptr_t>(x) >> 2) & 3);
+      const long long a0 = min(hi, lo + ((-(xmis + lo)) & 3));  // first 16-B-aligned key
+      const long long nv = (hi - a0) / 4;                       // float4s of the body
+      const long long a1 = a0 + 4 * nv;
+      if (tid < a0 - lo) hist_key(__float_as_uint(__ldg(x + lo + tid)));
+      if (tid < hi - a1) hist_key(__float_as_uint(__ldg(x + a1 + tid)));
+      const float4* x4 = reinterpret_cast<const float4*>(x + a0);
+      for (long long vb = 0; vb < nv; vb += 4 * kSelThreads) {
+        uint4 k4[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t key = keys[u];
-        const bool match = key != 0xffffffffu && ((key & pmask) == prefix);
-        const uint32_t digit = match ? ((key >> sh) & dmask) : 0xffffffffu;
-        const uint32_t grp = __match_any_sync(0xffffffffu, digit);
-        if (match) {
-          const uint64_t f = fixp(__uint_as_float(key));
-          const uint32_t s0 = __reduce_add_sync(grp, (uint32_t)(f & 0xFFFFF));
-          const uint32_t s1 = __reduce_add_sync(grp, (uint32_t)((f >> 20) & 0xFFFFF));
-          const uint32_t s2 = __reduce_add_sync(grp, (uint32_t)(f >> 40));
-          if ((__ffs(grp) - 1) == (int)lane_id()) {
-            atomicAdd(&sm.cnt[digit], (uint32_t)__popc(grp));
-            atomicAdd(&sm.mass[digit], ((unsigned long long)s2 << 40) +
-                                           ((unsigned long long)s1 << 20) + (unsigned long long)s0);
+        for (int u = 0; u < 4; ++u) {
+          const long long i = vb + u * kSelThreads + tid;
+          if (i < nv) {
+            const float4 f4 = __ldg(x4 + i);
+            k4[u] = make_uint4(__float_as_uint(f4.x), __float_as_uint(f4.y), __float_as_uint(f4.z),
+                               __float_as_uint(f4.w));
+          } else {
+            k4[u] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
           }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          hist_key(k4[u].x);
+          hist_key(k4[u].y);
+          hist_key(k4[u].z);
+          hist_key(k4[u].w);
         }
       }
     }
@@ -306,16 +348,52 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
       eq_run += cl_ld64(cl_map(&sm.slice_eq, r0 + r));
     }
   }
-  // ordered compaction of this slice
-  for (long long base = lo; base < hi; base += (long long)kSelThreads * kItems) {
+  // ordered compaction of this slice: the <= 3 keys before the first 16-B
+  // boundary by thread 0, then groups of kItems consecutive keys per thread
+  // from that boundary (two 16-B loads per full group)
+  const long long xmis = (long long)((reinterpret_cast<uintptr_t>(x) >> 2) & 3);
+  const long long a0 = min(hi, lo + ((-(xmis + lo)) & 3));
+  if (a0 > lo) {
+    if (tid == 0) {
+      uint64_t g = gt_run, q = eq_run;
+      for (long long i = lo; i < a0; ++i) {
+        const uint32_t key = __float_as_uint(__ldg(x + i));
+        if (key > lam) {
+          out[g + min(t_take, q)] = (int32_t)i;
+          ++g;
+        } else if (key == lam) {
+          if (q < t_take) out[g + q] = (int32_t)i;
+          ++q;
+        }
+      }
+      sm.above_cnt = g;  // free after the passes: broadcast slots
+      sm.above_mass = q;
+    }
+    __syncthreads();
+    gt_run = sm.above_cnt;
+    eq_run = sm.above_mass;
+    __syncthreads();
+  }
+  for (long long base = a0; base < hi; base += (long long)kSelThreads * kItems) {
     const long long i0 = base + (long long)tid * kItems;
     uint32_t keys[kItems];
     uint32_t gt = 0, eq = 0;
+    if (i0 + kItems <= hi) {
+#pragma unroll
+      for (int u = 0; u < kItems; u += 4) {
+        const float4 f4 = __ldg(reinterpret_cast<const float4*>(x + i0 + u));
+        keys[u] = __float_as_uint(f4.x);
+        keys[u + 1] = __float_as_uint(f4.y);
+        keys[u + 2] = __float_as_uint(f4.z);
+        keys[u + 3] = __float_as_uint(f4.w);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kItems; ++u) keys[u] = i0 + u < hi ? __float_as_uint(__ldg(x + i0 + u)) : 0u;
+    }
 #pragma unroll
     for (int u = 0; u < kItems; ++u) {
-      const long long i = i0 + u;
-      const bool valid = i < hi;
-      keys[u] = valid ? __float_as_uint(__ldg(x + i)) : 0u;
+      const bool valid = i0 + u < hi;
       gt += (valid && keys[u] > lam);
       eq += (valid && keys[u] == lam);
     }

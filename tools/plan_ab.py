@@ -65,10 +65,11 @@ for L in libs:
     plan(L)
     select(L)
     torch.cuda.synchronize()
-    outs.append((fpl.jsd.clone(), fpl.row_ptr.clone()))
+    outs.append((fpl.jsd.clone(), fpl.row_ptr.clone(), fpl.col_idx.clone()))
 for i in range(1, len(libs)):
     print(f"lib {i}: max |d jsd| {(outs[i][0] - outs[0][0]).abs().max().item():.2e}, "
-          f"row_ptr equal {torch.equal(outs[i][1], outs[0][1])}")
+          f"row_ptr equal {torch.equal(outs[i][1], outs[0][1])}, "
+          f"col_idx equal {torch.equal(outs[i][2], outs[0][2])}")
 res = {p: {"plan": [], "select": []} for p in a.libs}
 for _ in range(a.blocks):
     for p, L in zip(a.libs, libs):
