@@ -10,7 +10,10 @@
 
 namespace fp {
 
-constexpr int kChunkTilesMax = 8;  // key tiles (128 keys) per representative-pass CTA (max)
+#ifndef FP_CHUNK_TILES_MAX
+#define FP_CHUNK_TILES_MAX 8
+#endif
+constexpr int kChunkTilesMax = FP_CHUNK_TILES_MAX;  // key tiles (128 keys) per representative-pass CTA (max)
 #ifndef FP_MIN_CHUNKS
 #define FP_MIN_CHUNKS 16
 #endif

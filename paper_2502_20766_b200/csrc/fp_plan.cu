@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256) qbar_kernel(const __nv_bfloat16* __restri
   const int cnt = min(b, n - qb * b);
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const __nv_bfloat16* base = q + toff(ql, h, qb * b) + c8 * 8;
-#pragma unroll 4
+#pragma unroll 8
   for (int rr = 0; rr < rows; ++rr) {
     const int row = rg * rows + rr;
     if (row < cnt) {
