@@ -28,11 +28,15 @@ namespace fp {
 
 namespace {
 
-#ifndef FP_TOPMASS_AGG
-#define FP_TOPMASS_AGG 0  // 1: warp-aggregated histogram updates (round-2 kernel)
-#endif
 constexpr int kSelThreads = 1024;
-constexpr int kItems = 8;
+#ifdef FP_TM_TIMING
+// globaltimer (ns) at phase boundaries of topmass_segment, thread 0 of each CTA:
+// [head * 8 + cluster rank][phase] (tools/topmass_timing.py)
+__device__ unsigned long long g_tm_t[512][16];
+#define FP_TM(k) do { if (threadIdx.x == 0) { unsigned long long _t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t)); g_tm_t[blockIdx.y * 8 + blockIdx.x][k] = _t; } } while (0)
+#else
+#define FP_TM(k) do { } while (0)
+#endif
 constexpr float kFixScale = 1152921504606846976.0f;  // 2^60
 
 // x (>= 0, finite) in 2^-60 fixed point, truncated: floor(min(x, 8) * 2^60),
@@ -139,6 +143,7 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
   unsigned long long slice_gt = 0, slice_eq = 0;
   const int shifts[3] = {21, 10, 0};
   const int widths[3] = {11, 11, 10};
+  FP_TM(0);
   for (int pass = 0; pass < 3; ++pass) {
     const int sh = shifts[pass];
     const uint32_t dmask = (1u << widths[pass]) - 1u;
@@ -148,41 +153,50 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
       sm.mass[b] = 0;
     }
     __syncthreads();
+    FP_TM(1 + 4 * pass);
     // local histogram of the slice: 16-B loads of the 16-B-aligned body (4 in
     // flight per thread = 16 keys), the <= 3 keys before / after it scalar
+    // shared atomics per digit run (integer: order independent): the count
+    // an atomic add, the 64-bit fixed-point mass two native 32-bit adds on the
+    // halves of mass[digit] (little endian) with the carry of the low one (a
+    // 64-bit shared atomicAdd compiles to a CAS loop). Aggregating same-digit
+    // lanes of a warp first (match + partial-mask reductions, a loop over the
+    // warp's distinct digits) measured slower.
+    auto flush = [&](uint32_t digit, uint32_t c, uint64_t f) {
+      uint32_t* mh = reinterpret_cast<uint32_t*>(&sm.mass[digit]);
+      atomicAdd(&sm.cnt[digit], c);
+      const uint32_t lo = (uint32_t)f;
+      const uint32_t old = atomicAdd(mh, lo);
+      const uint32_t hi = (uint32_t)(f >> 32) + (old + lo < old ? 1u : 0u);
+      if (hi) atomicAdd(mh + 1, hi);
+    };
     auto hist_key = [&](uint32_t key) {
-      const bool match = key != 0xffffffffu && ((key & pmask) == prefix);
-#if FP_TOPMASS_AGG
-      const uint32_t digit = match ? ((key >> sh) & dmask) : 0xffffffffu;
-      const uint32_t grp = __match_any_sync(__activemask(), digit);
-      if (match) {
+      if (key != 0xffffffffu && (key & pmask) == prefix) flush((key >> sh) & dmask, 1u, fixp(__uint_as_float(key)));
+    };
+    // four adjacent keys of one thread: runs of equal digits are merged in
+    // registers first (neighbouring scores share a digit often: fewer
+    // same-address atomics, which the shared-memory unit serialises)
+    auto hist_key4 = [&](const uint4& k) {
+      const uint32_t kk[4] = {k.x, k.y, k.z, k.w};
+      uint32_t cd = 0xffffffffu, cc = 0;
+      uint64_t cm = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t key = kk[e];
+        if (key == 0xffffffffu || (key & pmask) != prefix) continue;
+        const uint32_t d = (key >> sh) & dmask;
         const uint64_t f = fixp(__uint_as_float(key));
-        const uint32_t s0 = __reduce_add_sync(grp, (uint32_t)(f & 0xFFFFF));
-        const uint32_t s1 = __reduce_add_sync(grp, (uint32_t)((f >> 20) & 0xFFFFF));
-        const uint32_t s2 = __reduce_add_sync(grp, (uint32_t)(f >> 40));
-        if ((__ffs(grp) - 1) == (int)lane_id()) {
-          atomicAdd(&sm.cnt[digit], (uint32_t)__popc(grp));
-          atomicAdd(&sm.mass[digit], ((unsigned long long)s2 << 40) +
-                                         ((unsigned long long)s1 << 20) + (unsigned long long)s0);
+        if (d == cd) {
+          ++cc;
+          cm += f;
+        } else {
+          if (cc) flush(cd, cc, cm);
+          cd = d;
+          cc = 1;
+          cm = f;
         }
       }
-#else
-      // shared atomics per matching key (integer: order independent) instead
-      // of aggregating same-digit lanes first (match + three partial-mask
-      // reductions, a loop over the warp's distinct digits): the count is a
-      // hardware-aggregated increment, the 64-bit mass two 32-bit adds on the
-      // halves of mass[digit] (little endian) with the carry of the low one
-      if (match) {
-        const uint32_t digit = (key >> sh) & dmask;
-        const uint64_t f = fixp(__uint_as_float(key));
-        uint32_t* mh = reinterpret_cast<uint32_t*>(&sm.mass[digit]);
-        atomicAdd(&sm.cnt[digit], 1u);
-        const uint32_t lo = (uint32_t)f;
-        const uint32_t old = atomicAdd(mh, lo);
-        const uint32_t hi = (uint32_t)(f >> 32) + (old + lo < old ? 1u : 0u);
-        if (hi) atomicAdd(mh + 1, hi);
-      }
-#endif
+      if (cc) flush(cd, cc, cm);
     };
     {
       const long long xmis = (long long)((reinterpret_cast<uintptr_t>(x) >> 2) & 3);
@@ -206,14 +220,10 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          hist_key(k4[u].x);
-          hist_key(k4[u].y);
-          hist_key(k4[u].z);
-          hist_key(k4[u].w);
-        }
+        for (int u = 0; u < 4; ++u) hist_key4(k4[u]);
       }
     }
+    FP_TM(2 + 4 * pass);
     if (nr > 1) {
       cl_sync();  // every CTA's local histogram is complete
       for (int b = tid; b < nbins; b += kSelThreads) {
@@ -246,6 +256,7 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
       }
       __syncthreads();
     }
+    FP_TM(3 + 4 * pass);
     if (pass == 0) {
       // total mass T from the first-digit histogram (exact, fixed point)
       unsigned long long tl = 0;
@@ -316,6 +327,7 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
     above_cnt_tot += sm.above_cnt;
     rem -= count_mode ? sm.above_cnt : sm.above_mass;
     __syncthreads();
+    FP_TM(4 + 4 * pass);
   }
   if (gamma >= 1.0f) {  // A7: everything, in index order
     for (long long i = lo + tid; i < hi; i += kSelThreads) out[i] = (int32_t)i;
@@ -348,9 +360,9 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
       eq_run += cl_ld64(cl_map(&sm.slice_eq, r0 + r));
     }
   }
+  FP_TM(13);
   // ordered compaction of this slice: the <= 3 keys before the first 16-B
-  // boundary by thread 0, then groups of kItems consecutive keys per thread
-  // from that boundary (two 16-B loads per full group)
+  // boundary by thread 0, then a contiguous range per thread from that boundary
   const long long xmis = (long long)((reinterpret_cast<uintptr_t>(x) >> 2) & 3);
   const long long a0 = min(hi, lo + ((-(xmis + lo)) & 3));
   if (a0 > lo) {
@@ -374,53 +386,66 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
     eq_run = sm.above_mass;
     __syncthreads();
   }
-  for (long long base = a0; base < hi; base += (long long)kSelThreads * kItems) {
-    const long long i0 = base + (long long)tid * kItems;
-    uint32_t keys[kItems];
-    uint32_t gt = 0, eq = 0;
-    if (i0 + kItems <= hi) {
-#pragma unroll
-      for (int u = 0; u < kItems; u += 4) {
-        const float4 f4 = __ldg(reinterpret_cast<const float4*>(x + i0 + u));
-        keys[u] = __float_as_uint(f4.x);
-        keys[u + 1] = __float_as_uint(f4.y);
-        keys[u + 2] = __float_as_uint(f4.z);
-        keys[u + 3] = __float_as_uint(f4.w);
-      }
+  // thread t owns the keys [a0 + t P, a0 + (t + 1) P) (P a multiple of 4:
+  // 16-B loads): one pass counts its keys > lambda / == lambda, ONE block scan
+  // gives every thread its output offset, a second pass over the same keys
+  // (L1 / L2 resident) writes the selected indices in index order. (Rounds of
+  // 8 consecutive keys per thread with a scan each -- also with the output
+  // staged in shared memory for coalesced stores -- and four loads in flight
+  // per thread here measured slower: profiles/r02s3_topmass_phases.txt.)
+  const long long P = 4 * ((hi - a0 + 4LL * kSelThreads - 1) / (4LL * kSelThreads));
+  const long long b0 = min(hi, a0 + (long long)tid * P), b1 = min(hi, b0 + P);
+  auto load4 = [&](long long i, uint32_t* kk) {
+    if (i + 4 <= b1) {
+      const float4 f4 = __ldg(reinterpret_cast<const float4*>(x + i));
+      kk[0] = __float_as_uint(f4.x);
+      kk[1] = __float_as_uint(f4.y);
+      kk[2] = __float_as_uint(f4.z);
+      kk[3] = __float_as_uint(f4.w);
     } else {
 #pragma unroll
-      for (int u = 0; u < kItems; ++u) keys[u] = i0 + u < hi ? __float_as_uint(__ldg(x + i0 + u)) : 0u;
+      for (int e = 0; e < 4; ++e) kk[e] = i + e < b1 ? __float_as_uint(__ldg(x + i + e)) : 0u;
     }
+  };
+  uint32_t gt = 0, eq = 0;
+  for (long long i = b0; i < b1; i += 4) {
+    uint32_t kk[4];
+    load4(i, kk);
 #pragma unroll
-    for (int u = 0; u < kItems; ++u) {
-      const bool valid = i0 + u < hi;
-      gt += (valid && keys[u] > lam);
-      eq += (valid && keys[u] == lam);
+    for (int e = 0; e < 4; ++e) {
+      const bool valid = i + e < b1;
+      gt += (valid && kk[e] > lam);
+      eq += (valid && kk[e] == lam);
     }
+  }
+  {
     uint64_t tot;
     const uint64_t packed = ((uint64_t)eq << 32) | gt;
     const uint64_t excl = block_scan_u64(packed, sm.wsum, &tot) - packed;
     uint64_t eq_pre = eq_run + (excl >> 32);
     uint64_t pos = gt_run + (excl & 0xffffffffu) + min(t_take, eq_pre);
+    for (long long i = b0; i < b1; i += 4) {
+      uint32_t kk[4];
+      load4(i, kk);
 #pragma unroll
-    for (int u = 0; u < kItems; ++u) {
-      const long long i = i0 + u;
-      if (i >= hi) break;
-      bool take = keys[u] > lam;
-      if (keys[u] == lam) {
-        take = eq_pre < t_take;
-        ++eq_pre;
+      for (int e = 0; e < 4; ++e) {
+        if (i + e >= b1) break;
+        bool take = kk[e] > lam;
+        if (kk[e] == lam) {
+          take = eq_pre < t_take;
+          ++eq_pre;
+        }
+        if (take) out[pos++] = (int32_t)(i + e);
       }
-      if (take) out[pos++] = (int32_t)i;
     }
-    gt_run += tot & 0xffffffffu;
-    eq_run += tot >> 32;
   }
+  FP_TM(14);
   if (tid == 0 && sub == 0) {
     *count_out = (int32_t)K;
     *mass_out = above_mass_tot + t_take * f_lam;
   }
   if (nr > 1) cl_sync();  // keep this CTA's shared memory alive until the sub-group is done
+  FP_TM(15);
 }
 
 // One cluster of C CTAs (1, 2, 4 or 8; set at launch) per head. VS head:
@@ -1042,3 +1067,9 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
 }
 
 }  // namespace fp
+
+#ifdef FP_TM_TIMING
+extern "C" int fp_debug_topmass_timing(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, fp::g_tm_t, sizeof(fp::g_tm_t));
+}
+#endif
