@@ -17,8 +17,8 @@
 //
 // One CTA per (head, q-block pair (qbA, qbB = qbA - 1)) work item, 384 threads:
 //   warp 8   K producer   Q_A, Q_B tiles, then the K tiles of the union list
-//                         (merge of the two sorted CSR rows) into a 2-stage ring
-//   warp 10  V producer   the V tiles of the union list into a 3-stage ring
+//                         (merge of the two sorted CSR rows) into a 3-stage ring
+//   warp 10  V producer   the V tiles of the union list into a 2-stage ring
 //   warp 9   MMA issuer   per union entry e and stream X in (A, B): first the
 //                         pending O_X += P_X V (X's previous entry), then, if X
 //                         selected e, S_X = Q_X K_e^T (both operands in smem,
@@ -65,7 +65,18 @@ namespace fp {
 namespace {
 
 constexpr int kThreads8 = 384;
-constexpr int kKS8 = 2, kVS8 = 3;  // K / V ring depths (tiles)
+// K / V ring depths (tiles). A V slot is released by the entry's last PV,
+// which the issuer sends no later than the next union entry, so two V slots
+// cannot deadlock; the third K slot gives the K loads a second entry of lead
+// (3 / 2 measured bitwise equal and 0.2-2% faster than 2 / 3 at C3, C4, C5
+// 16k and dense: profiles/r02s3_attn_kv_ring_ab.txt)
+#ifndef FP_KS8
+#define FP_KS8 3
+#endif
+#ifndef FP_VS8
+#define FP_VS8 2
+#endif
+constexpr int kKS8 = FP_KS8, kVS8 = FP_VS8;
 constexpr uint32_t kColS8 = 0, kColO8 = 256;
 constexpr float kRescale8 = 8.0f;  // lazy rescale: tolerate P up to 2^8 (as v5)
 // a row sum above 2^64 (some P may exceed 2^64 against the row's reference)
