@@ -77,6 +77,10 @@ constexpr int kThreads8 = 384;
 #define FP_VS8 2
 #endif
 constexpr int kKS8 = FP_KS8, kVS8 = FP_VS8;
+#ifndef FP_PV3
+#define FP_PV3 1
+#endif
+constexpr bool kPv3 = FP_PV3 != 0;  // PV in three steps: keys 0-63 (p_lo), 64-95 (p_mid), 96-127 (p_full)
 constexpr uint32_t kColS8 = 0, kColO8 = 256;
 constexpr float kRescale8 = 8.0f;  // lazy rescale: tolerate P up to 2^8 (as v5)
 // a row sum above 2^64 (some P may exceed 2^64 against the row's reference)
@@ -107,7 +111,7 @@ struct Attn8Smem {
   int item[2];
   uint64_t k_full[kKS8], k_empty[kKS8];
   uint64_t v_full[kVS8], v_empty[kVS8];
-  uint64_t s_full[2], p_full[2], p_lo[2], pv_done[2];
+  uint64_t s_full[2], p_full[2], p_lo[2], p_mid[2], pv_done[2];
   uint32_t tmem_base;
   // exact redo of flagged work items (see the fetcher): ring written by the
   // softmax warps, read by the fetcher; per-item dedupe flags; completed
@@ -180,6 +184,14 @@ FP_DEV void umma_pv_chain4_w(uint32_t d, uint32_t a0, uint64_t b0, uint32_t ides
       "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %8, %9, p;\n\t}" ::"r"(d),
       "r"(a0), "r"(a0 + 8), "r"(a0 + 16), "r"(a0 + 24), "l"(b0), "l"(b0 + 128), "l"(b0 + 256),
       "l"(b0 + 384), "r"(idesc), "r"(acc0));
+}
+// two PV k-steps (accumulating), K = 16 keys each
+FP_DEV void umma_pv_chain2_w(uint32_t d, uint32_t a0, uint64_t b0, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, ep;\n\tsetp.ne.b32 p, 1, 0;\n\t" FP_ELECT
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, p;\n\t"
+      "@ep tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %4, %5, p;\n\t}" ::"r"(d),
+      "r"(a0), "r"(a0 + 8), "l"(b0), "l"(b0 + 128), "r"(idesc));
 }
 FP_DEV void umma_commit_w(uint64_t* bar) {
   asm volatile(
@@ -421,6 +433,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
       mbar_init(&sm.s_full[x], 1);
       mbar_init(&sm.p_full[x], 4);  // one arrival per softmax warp of the stream
       mbar_init(&sm.p_lo[x], 4);
+      mbar_init(&sm.p_mid[x], 4);
       mbar_init(&sm.pv_done[x], 1);
     }
     mbar_fence_init();
@@ -555,6 +568,11 @@ __global__ void __launch_bounds__(kThreads8, 1)
             tc_fence_after();
             PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128, vdesc, idesc_o, lcnt[x] > 1);
             FP_T8(12);
+            if (kPv3) {  // k-steps 4-5 (keys 64-95) on p_mid
+              mbar_wait(&sm.p_mid[x], (cnt[x] - 1) & 1);
+              tc_fence_after();
+              umma_pv_chain2_w(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512, idesc_o);
+            }
             mbar_wait(&sm.p_full[x], (cnt[x] - 1) & 1);
             FP_T8(11);
 #ifdef FP_TIMING
@@ -563,7 +581,11 @@ __global__ void __launch_bounds__(kThreads8, 1)
             }
 #endif
             tc_fence_after();
-            PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512, idesc_o, 1);
+            if (kPv3) {
+              umma_pv_chain2_w(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 48, vdesc + 768, idesc_o);
+            } else {
+              PVCHAIN4(tbase + kColO8 + x * 128, tbase + kColS8 + x * 128 + 32, vdesc + 512, idesc_o, 1);
+            }
             COMMIT8(&sm.v_empty[vs]);
             COMMIT8(&sm.pv_done[x]);
             pend[x] = -1;
@@ -655,7 +677,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
         // experiment: softmax does no work (measures the MMA/issuer pipeline alone)
         tc_fence_after();
         __syncwarp();
-        if (lane_id() == 0) { mbar_arrive(&sm.p_lo[x]); mbar_arrive(&sm.p_full[x]); }
+        if (lane_id() == 0) { mbar_arrive(&sm.p_lo[x]); if (kPv3) mbar_arrive(&sm.p_mid[x]); mbar_arrive(&sm.p_full[x]); }
         continue;
 #endif
         tc_fence_after();
@@ -760,6 +782,14 @@ __global__ void __launch_bounds__(kThreads8, 1)
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(&sm.p_lo[x]);
             FP_T8(4);
+          }
+          if (kPv3 && ch == 3) {
+            // p_mid after chunk 3's exponentials: chunk 2 is stored, the
+            // issuer runs PV k-steps 4-5 while chunk 3 is stored
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&sm.p_mid[x]);
           }
           tmem_st16(tS + ch * 16, pk);  // P over S: 32 keys = 16 columns of bf16 pairs
         }
