@@ -13,7 +13,8 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
                       "regex:" + kern], capture_output=True, text=True).stdout
 lines = out.splitlines()
-rows = list(csv.DictReader(io.StringIO("\n".join(lines[1:]))))
+rows = [r for r in csv.DictReader(io.StringIO("\n".join(lines[1:])))
+        if (r.get("Warp Stall Sampling (All Samples)") or "0").isdigit()]  # one block per matching kernel
 tot = sum(int(r["Warp Stall Sampling (All Samples)"] or 0) for r in rows)
 print(f"{len(rows)} SASS lines, {tot} stall samples")
 key = lambda r: int(r["Warp Stall Sampling (All Samples)"] or 0)
