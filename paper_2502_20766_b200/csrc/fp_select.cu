@@ -81,6 +81,10 @@ __device__ uint64_t block_scan_u64(uint64_t v, uint64_t* wsum, uint64_t* total) 
 }
 
 constexpr int kClMax = 8;  // max CTAs (one cluster) per head; chosen per launch
+#ifndef FP_TOP_MIN_KEYS
+#define FP_TOP_MIN_KEYS 16384
+#endif
+constexpr long long kTopMinKeys = FP_TOP_MIN_KEYS;  // scores per CTA below which more CTAs do not pay
 
 // distributed shared memory helpers (thread block cluster)
 __device__ __forceinline__ uint32_t cl_rank() {
@@ -999,6 +1003,15 @@ cudaError_t launch_select(const Shape& s, const WsLayout& L, void* ws, float gam
     long long need = std::max((lqa + 159999) / 160000, 2 * ((lvs + 79999) / 80000));
     int ncl = 1;
     while (ncl < need && ncl < kClMax) ncl <<= 1;
+    // more CTAs per head while the whole grid still fits in one wave (one
+    // 1024-thread CTA per SM) and a VS CTA keeps >= kTopMinKeys scores: the
+    // histogram passes scale with the slice, the barriers and scans do not
+    {
+      int nsm = 148, dev = 0;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      // (a VS segment gets ncl / 2 CTAs: after doubling, lvs / ncl scores each)
+      while (ncl < kClMax && (long long)s.H * ncl * 2 <= nsm && lvs / ncl >= kTopMinKeys) ncl <<= 1;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ncl, s.H);
     cfg.blockDim = dim3(kSelThreads);
