@@ -77,6 +77,18 @@ constexpr int kThreads8 = 384;
 #define FP_VS8 2
 #endif
 constexpr int kKS8 = FP_KS8, kVS8 = FP_VS8;
+// per-lane registers after setmaxnreg: producer / issuer warpgroup (dec) and
+// the two softmax warpgroups (inc); the launch holds 12 warps x 168, so
+// 4 x DEC + 8 x INC must stay <= 2016 (88 / 208, or 104 / 200)
+#ifndef FP_DECREG8
+#define FP_DECREG8 88
+#endif
+#ifndef FP_INCREG8
+#define FP_INCREG8 208
+#endif
+static_assert(4 * FP_DECREG8 + 8 * FP_INCREG8 <= 12 * 168, "setmaxnreg budget");
+#define FP_STR8_(x) #x
+#define FP_STR8(x) FP_STR8_(x)
 #ifndef FP_PV3
 #define FP_PV3 1
 #endif
@@ -458,7 +470,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
   };
 
   if (wid >= 8) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 " FP_STR8(FP_DECREG8) ";");
     if (wid == 8 || wid == 10) {
       // ------------------------------------------------ TMA producers (K: warp 8, V: warp 10)
       if (lane_id() == 0) {
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(kThreads8, 1)
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 " FP_STR8(FP_INCREG8) ";");
     // ------------------------------------------------ softmax warpgroups
     const int x = wid >> 2;                     // 0 = row A, 1 = row B
     const int r = (wid & 3) * 32 + lane_id();   // query row within the block = TMEM lane
