@@ -177,15 +177,15 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
     auto hist_key = [&](uint32_t key) {
       if (key != 0xffffffffu && (key & pmask) == prefix) flush((key >> sh) & dmask, 1u, fixp(__uint_as_float(key)));
     };
-    // four adjacent keys of one thread: runs of equal digits are merged in
+    // eight adjacent keys of one thread: runs of equal digits are merged in
     // registers first (neighbouring scores share a digit often: fewer
     // same-address atomics, which the shared-memory unit serialises)
-    auto hist_key4 = [&](const uint4& k) {
-      const uint32_t kk[4] = {k.x, k.y, k.z, k.w};
+    auto hist_keys = [&](const uint4& k, const uint4& k2) {
+      const uint32_t kk[8] = {k.x, k.y, k.z, k.w, k2.x, k2.y, k2.z, k2.w};
       uint32_t cd = 0xffffffffu, cc = 0;
       uint64_t cm = 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < 8; ++e) {
         const uint32_t key = kk[e];
         if (key == 0xffffffffu || (key & pmask) != prefix) continue;
         const uint32_t d = (key >> sh) & dmask;
@@ -211,10 +211,12 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
       if (tid < hi - a1) hist_key(__float_as_uint(__ldg(x + a1 + tid)));
       const float4* x4 = reinterpret_cast<const float4*>(x + a0);
       for (long long vb = 0; vb < nv; vb += 4 * kSelThreads) {
+        // thread t: float4s 2t, 2t + 1 and 2048 + 2t, 2048 + 2t + 1 of the
+        // step (eight adjacent keys per run merge)
         uint4 k4[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const long long i = vb + u * kSelThreads + tid;
+          const long long i = vb + (u >> 1) * 2 * kSelThreads + 2 * tid + (u & 1);
           if (i < nv) {
             const float4 f4 = __ldg(x4 + i);
             k4[u] = make_uint4(__float_as_uint(f4.x), __float_as_uint(f4.y), __float_as_uint(f4.z),
@@ -223,8 +225,8 @@ __device__ void topmass_segment(TopSmem& sm, const float* __restrict__ x, long l
             k4[u] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
           }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) hist_key4(k4[u]);
+        hist_keys(k4[0], k4[1]);
+        hist_keys(k4[2], k4[3]);
       }
     }
     FP_TM(2 + 4 * pass);
