@@ -220,3 +220,34 @@ def test_layer_host_invalid_call_enqueues_nothing(fp):
     torch.cuda.synchronize()
     assert bool((dq == 7.0).all()) and bool((dk == 7.0).all()) and bool((do == 7.0).all())
     assert bool((oh == 0).all())
+
+
+def test_head_slices_csr_bitwise_64k(fp):
+    """The top-mass cluster size depends on how many heads a call batches (more
+    CTAs per head while the grid fits one wave: C = 4 for the 32-head layer, 8
+    for one head or one KV group at 64k); the selection is exact integer
+    arithmetic over the same scores, so the CSR (row_ptr AND col_idx) of a head
+    must not depend on it (head-partitioned multi-GPU runs rely on this)."""
+    import torch
+    w = C2.with_(seq_len=65536)
+    q, k, _ = gen.make_layer_bits(w)
+    full = fp.FlexPrefill(w.heads, w.kv_heads, w.seq_len)
+    qa = torch.from_numpy(q).view(torch.bfloat16).cuda()
+    ka = torch.from_numpy(k).view(torch.bfloat16).cuda()
+    full.plan(qa, ka, w.tau)
+    full.select(w.gamma, w.min_budget)
+    torch.cuda.synchronize()
+    rp_all, ci_all = full.row_ptr.cpu().numpy(), full.col_idx.cpu().numpy()
+    g = w.heads // w.kv_heads
+    for h0, nh, kv0, nkv in ((3, 1, 0, 1), (12, g, 3, 1)):
+        f1 = fp.FlexPrefill(nh, nkv, w.seq_len)
+        qt = torch.from_numpy(q[h0:h0 + nh]).view(torch.bfloat16).cuda()
+        kt = torch.from_numpy(k[kv0:kv0 + nkv]).view(torch.bfloat16).cuda()
+        f1.plan(qt, kt, w.tau)
+        f1.select(w.gamma, w.min_budget)
+        torch.cuda.synchronize()
+        rp, ci = f1.row_ptr.cpu().numpy(), f1.col_idx.cpu().numpy()
+        assert np.array_equal(rp, rp_all[h0:h0 + nh]), (h0, nh)
+        for j in range(nh):
+            nnz = int(rp[j, -1])
+            assert np.array_equal(ci[j, :nnz], ci_all[h0 + j, :nnz]), (h0 + j)
